@@ -1,0 +1,92 @@
+/*
+ * swarm_am.h -- C ABI of the B200 alternating-minimization (AM) joint
+ * multi-agent trajectory solver (drop-in for the reference's solve path).
+ *
+ * The reference (pkg/src/swarmtraj, pure Python) has no FFI; its seams are
+ * Python calls.  Each entry point below replaces one of them:
+ *
+ *   st_plan_create   <- FactorCache.prefactorize + KktFactor construction
+ *                       (kkt_cache.py:332-353, 421-456): uploads the per-stage
+ *                       structured KKT operators (kkt.py) once per fingerprint.
+ *   st_solve         <- am_solve's loop (solver.py:405-457) for one scenario or a
+ *                       batch sharing one fingerprint (bench.py:120-158 runs the
+ *                       same batch through threads).  Host buffers in/out.
+ *   st_solve_device  <- same, device buffers, caller's stream (HBM-resident batches).
+ *   st_plan_destroy  <- releasing a cache entry.
+ *   st_last_error    <- the ValueError/RuntimeError text of the failed call.
+ *
+ * Conventions: all arrays are C-contiguous float64 (or int32), caller-owned.
+ * Layouts follow the reference: coefficients (3, n, nv) per scenario
+ * (SolveReport.coefficients, solver.py:146), boundary rows (3, n, 6) in the
+ * order [pos0, vel0, acc0, posT, velT, accT] (kkt_cache.py:174-185),
+ * multipliers (3, p, m) pair-major with agent pairs (i<j) lexicographic then
+ * (agent, obstacle) agent-major (kkt_cache.py:197-215).
+ * Return value: 0 ok; ST_EINVAL bad argument; ST_ECUDA CUDA failure;
+ * ST_ENOMEM device allocation failure; ST_EUNSUPPORTED shape outside the
+ * compiled kernels.  Plans are safe to share between threads (calls on one
+ * plan serialize).
+ */
+#ifndef SWARM_AM_H
+#define SWARM_AM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_OK 0
+#define ST_EINVAL 1
+#define ST_ECUDA 2
+#define ST_ENOMEM 3
+#define ST_EUNSUPPORTED 4
+
+#define ST_FLAG_KEEP_STATE 1 /* write final multipliers/d (batch must be 1) */
+
+typedef struct st_plan st_plan;
+
+/* Per-fingerprint operators.  P: m x nv sampled basis.  For each of the
+ * n_stages rho values: G, Gm (nv x nv) and F, Fm (nv x 6) -- see kkt.py for
+ * their definition from the 17x17 K_dev / K_mean blocks.  E: 6 x nv endpoint
+ * rows.  rho: n_stages penalty weights.  device: CUDA ordinal. */
+int st_plan_create(int n_agents, int n_obstacles, int n_samples, int n_coeffs, int n_stages,
+                   const double* P, const double* G, const double* Gm, const double* F,
+                   const double* Fm, const double* E, const double* rho, int device,
+                   st_plan** out);
+
+int st_plan_destroy(st_plan* plan);
+
+/* Solve `batch` scenarios (host pointers).
+ *   c0     batch x 3 x n x nv   straight-line initial coefficients
+ *   b_eq   batch x 3 x n x 6    boundary rows
+ *   geom   batch x (2 + 5*n_obs): agent l_xy, l_z, then per obstacle
+ *          (cx, cy, cz, l_xy, l_z) with the agent-obstacle semi-axes
+ *   switch_every, max_iters, tol: the rho schedule and stopping rule
+ *   cluster_hint: CTAs per scenario (0 = choose)
+ * Outputs: c_out (batch x 3 x n x nv), hist (batch x 3 x max_iters:
+ * residual norm, residual max-abs, boundary max per iteration), iters,
+ * converged (batch).  lam_out (3 x p x m) and d_out (p x m) only with
+ * ST_FLAG_KEEP_STATE, else may be NULL.  timings_ms (may be NULL):
+ * [h2d, device loop, d2h]. */
+int st_solve(st_plan* plan, int batch, const double* c0, const double* b_eq, const double* geom,
+             int switch_every, int max_iters, double tol, int flags, int cluster_hint,
+             double* c_out, double* hist, int* iters, int* converged, double* lam_out,
+             double* d_out, float* timings_ms);
+
+/* Same contract, every array a device pointer, enqueued on `stream`
+ * (a cudaStream_t, NULL = the plan's stream); no host synchronization. */
+int st_solve_device(st_plan* plan, int batch, const double* c0, const double* b_eq,
+                    const double* geom, int switch_every, int max_iters, double tol, int flags,
+                    int cluster_hint, double* c_out, double* hist, int* iters, int* converged,
+                    double* lam_out, double* d_out, void* stream);
+
+/* Launch configuration st_solve would use: out[0..7] = cluster size C,
+ * agent blocks NB, lane segment width W, threads per CTA, lambda-in-smem flag,
+ * dynamic smem bytes, clusters launched, steps per warp task. */
+int st_query_launch(st_plan* plan, int batch, int cluster_hint, long long* out8);
+
+const char* st_last_error(void);
+int st_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWARM_AM_H */

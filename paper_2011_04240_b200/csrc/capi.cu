@@ -1,0 +1,414 @@
+// C ABI of the B200 AM solver (declared in include/swarm_am.h): plan upload,
+// launch-configuration choice and the host/device solve entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/swarm_am.h"
+#include "am_kernel.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define ST_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      return fail(e_ == cudaErrorMemoryAllocation ? ST_ENOMEM : ST_ECUDA,                     \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                         \
+    }                                                                                          \
+  } while (0)
+
+using KernelFn = void (*)(swarm::KParams);
+
+struct KernelEntry {
+  int NB, NT;
+  KernelFn fn;
+};
+
+const KernelEntry kKernels[] = {
+    {1, 512, swarm::am_cluster_kernel<1, 512>},
+    {2, 512, swarm::am_cluster_kernel<2, 512>},
+    {4, 256, swarm::am_cluster_kernel<4, 256>},
+    {8, 256, swarm::am_cluster_kernel<8, 256>},
+};
+
+struct Launch {
+  int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
+  int lam_smem = 0, nclusters = 0;
+  size_t smem_bytes = 0;
+  long long lam_per_cta = 0;
+  KernelFn fn = nullptr;
+  swarm::KParams kp{};
+};
+
+}  // namespace
+
+struct st_plan {
+  int n, nobs, m, nv, S, device;
+  double* d_mats = nullptr;  // P | G | Gm | F | Fm | E | rho
+  const double *P, *G, *Gm, *F, *Fm, *E, *rho;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int* d_counter = nullptr;
+  double* d_lam = nullptr;
+  size_t lam_bytes = 0;
+  void* d_io = nullptr;  // inputs+outputs of host-pointer solves
+  size_t io_bytes = 0;
+  int smem_optin = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Steps of one warp task; mirrors the enumeration in pairwise_phase().
+int count_steps(int n, int nobs, int NB) {
+  if (NB == 1) return n / 2 + nobs;
+  int st = 0;
+  for (int A = 0; A < NB; ++A) {
+    const int nA = std::min(32, n - A * 32);
+    if (nA <= 0) continue;
+    st += nA / 2 + nobs;
+  }
+  for (int A = 0; A < NB; ++A)
+    for (int B = A + 1; B < NB; ++B)
+      if (std::min(32, n - B * 32) > 0) st += 32;
+  return st;
+}
+
+// Shared-memory carve-up for cluster size C; returns total doubles (lambda excluded).
+long long layout(st_plan* pl, Launch& L, int C) {
+  swarm::KParams& k = L.kp;
+  const int NP = L.NB * 32, nv = pl->nv, n = pl->n;
+  L.C = C;
+  L.tmax = ceil_div(pl->m, C);
+  L.tasks_max = ceil_div(L.tmax, 32 / L.W);
+  L.own_max = ceil_div(n, C);
+  long long o = 0;
+  auto take = [&](int& off, long long cnt) {
+    off = (int)o;
+    o += (cnt + 1) & ~1LL;  // keep 16-byte alignment
+  };
+  take(k.o_c, 3LL * n * nv);
+  take(k.o_X, 3LL * L.tmax * NP);
+  take(k.o_q, 3LL * L.tmax * NP);
+  take(k.o_P, (long long)L.tmax * nv);
+  take(k.o_r1, (long long)C * L.own_max * 3 * nv);
+  take(k.o_rS, (long long)C * 3 * nv);
+  take(k.o_rN, 2LL * C);
+  take(k.o_rB, C);
+  take(k.o_R, (long long)L.own_max * 3 * nv);
+  take(k.o_Rb, 3LL * nv);
+  take(k.o_cl, (long long)L.own_max * 3 * nv);
+  take(k.o_gap, 18LL * L.own_max);
+  take(k.o_geo, 2 + 5LL * pl->nobs);
+  take(k.o_beq, 18LL * L.own_max);
+  take(k.o_bb, 18);
+  take(k.o_wp, 2LL * (L.NT / 32));
+  take(k.o_misc, 2);
+  k.o_lam = (int)o;
+  L.lam_per_cta = (long long)L.tasks_max * L.nsteps * 96;
+  return o;
+}
+
+int choose_launch(st_plan* pl, int batch, int hint, Launch& L) {
+  const int n = pl->n;
+  if (n < 1 || n > 256) return fail(ST_EUNSUPPORTED, "n_agents must be in [1, 256] for the compiled kernels");
+  if (pl->nv > 16) return fail(ST_EUNSUPPORTED, "n_coeffs must be <= 16 (degree <= 15)");
+  const int nb_need = n <= 32 ? 1 : ceil_div(n, 32);
+  const KernelEntry* ke = nullptr;
+  for (const auto& e : kKernels)
+    if (e.NB >= nb_need) { ke = &e; break; }
+  if (!ke) return fail(ST_EUNSUPPORTED, "no kernel for this agent count");
+  L.NB = ke->NB;
+  L.NT = ke->NT;
+  L.fn = ke->fn;
+  if (L.NB == 1) {
+    int w = 2;
+    while (w < n) w <<= 1;
+    L.W = w;
+  } else {
+    L.W = 32;
+  }
+  L.nsteps = count_steps(n, pl->nobs, L.NB);
+  const long long budget = pl->smem_optin / 8;
+
+  ST_CUDA(cudaFuncSetAttribute(L.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  std::vector<int> cands;
+  if (hint > 0) {
+    cands.push_back(hint);
+  } else if (batch == 1) {
+    cands = {16, 8, 4, 2, 1};
+  } else {
+    cands = {1, 2, 4, 8, 16};
+  }
+  // pass 0: lambda in smem (throughput order: smallest C that fits; latency order: largest C)
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int C : cands) {
+      if (C > pl->m || C < 1 || C > 16) continue;
+      Launch T = L;
+      const long long base = layout(pl, T, C);
+      const bool fits = base + T.lam_per_cta <= budget;
+      if (pass == 0 && !fits) continue;
+      if (base > budget) continue;
+      T.lam_smem = fits ? 1 : 0;
+      T.smem_bytes = (size_t)(base + (T.lam_smem ? T.lam_per_cta : 0)) * 8;
+      ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_bytes));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(T.NT);
+      cfg.dynamicSmemBytes = T.smem_bytes;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int active = 0;
+      cudaError_t e = cudaOccupancyMaxActiveClusters(&active, (void*)T.fn, &cfg);
+      if (e != cudaSuccess || active < 1) {
+        cudaGetLastError();
+        continue;
+      }
+      T.nclusters = std::min(batch, active);
+      L = T;
+      return 0;
+    }
+  }
+  return fail(ST_EUNSUPPORTED, "no cluster configuration fits this problem on the device");
+}
+
+int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double* beq, const double* geom,
+        int switch_every, int max_iters, double tol, int flags, double* c_out, double* hist, int* iters,
+        int* conv, double* lam_out, double* d_out, cudaStream_t s) {
+  Launch L = L0;
+  swarm::KParams& k = L.kp;
+  k.n = pl->n; k.nobs = pl->nobs; k.m = pl->m; k.nv = pl->nv; k.S = pl->S;
+  k.P = pl->P; k.G = pl->G; k.Gm = pl->Gm; k.F = pl->F; k.Fm = pl->Fm; k.E = pl->E; k.rho = pl->rho;
+  k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
+  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta;
+  k.B = batch; k.gstride = 2 + 5 * pl->nobs;
+  k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
+  k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
+  k.switch_every = switch_every; k.max_iters = max_iters; k.flags = flags; k.tol = tol;
+  if (!L.lam_smem) {
+    const size_t need = (size_t)L.nclusters * L.C * L.lam_per_cta * sizeof(double);
+    if (need > pl->lam_bytes) {
+      if (pl->d_lam) cudaFree(pl->d_lam);
+      pl->d_lam = nullptr;
+      pl->lam_bytes = 0;
+      ST_CUDA(cudaMalloc(&pl->d_lam, need));
+      pl->lam_bytes = need;
+    }
+    k.lam_ws = pl->d_lam;
+  } else {
+    k.lam_ws = nullptr;
+  }
+  ST_CUDA(cudaMemsetAsync(pl->d_counter, 0, sizeof(int), s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.nclusters * L.C);
+  cfg.blockDim = dim3(L.NT);
+  cfg.dynamicSmemBytes = L.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = L.C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ST_CUDA(cudaLaunchKernelEx(&cfg, L.fn, k));
+  return 0;
+}
+
+int check_common(st_plan* pl, int batch, int switch_every, int max_iters, double tol, int flags) {
+  if (!pl) return fail(ST_EINVAL, "plan is NULL");
+  if (batch < 1) return fail(ST_EINVAL, "batch must be >= 1");
+  if (switch_every < 1) return fail(ST_EINVAL, "switch_every must be >= 1");
+  if (max_iters < 1) return fail(ST_EINVAL, "max_iters must be >= 1");
+  if (!(tol > 0)) return fail(ST_EINVAL, "tolerance must be positive");
+  if ((flags & ST_FLAG_KEEP_STATE) && batch != 1) return fail(ST_EINVAL, "keep_state needs batch == 1");
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int st_version(void) { return 1; }
+
+const char* st_last_error(void) { return g_err.c_str(); }
+
+int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const double* G, const double* Gm,
+                   const double* F, const double* Fm, const double* E, const double* rho, int device,
+                   st_plan** out) {
+  if (!out) return fail(ST_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || nobs < 0 || m < 2 || nv < 6 || S < 1)
+    return fail(ST_EINVAL, "bad dimensions (need n>=1, n_obs>=0, m>=2, nv>=6, stages>=1)");
+  if (!P || !G || !Gm || !F || !Fm || !E || !rho) return fail(ST_EINVAL, "NULL operator pointer");
+  int ndev = 0;
+  ST_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ST_EINVAL, "device ordinal out of range");
+  ST_CUDA(cudaSetDevice(device));
+  st_plan* pl = new st_plan();
+  pl->n = n; pl->nobs = nobs; pl->m = m; pl->nv = nv; pl->S = S; pl->device = device;
+  const size_t nP = (size_t)m * nv, nG = (size_t)S * nv * nv, nF = (size_t)S * nv * 6, nE = 6 * (size_t)nv;
+  const size_t total = nP + 2 * nG + 2 * nF + nE + S;
+  std::vector<double> h(total);
+  size_t o = 0;
+  auto put = [&](const double* src, size_t cnt) {
+    std::memcpy(h.data() + o, src, cnt * sizeof(double));
+    o += cnt;
+  };
+  put(P, nP); put(G, nG); put(Gm, nG); put(F, nF); put(Fm, nF); put(E, nE); put(rho, S);
+  auto cleanup = [&](int code) {
+    if (pl->d_mats) cudaFree(pl->d_mats);
+    if (pl->d_counter) cudaFree(pl->d_counter);
+    if (pl->stream) cudaStreamDestroy(pl->stream);
+    delete pl;
+    return code;
+  };
+  cudaError_t e = cudaMalloc(&pl->d_mats, total * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(pl->d_mats, h.data(), total * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&pl->d_counter, sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&pl->ev[i]);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) {
+    fail(e == cudaErrorMemoryAllocation ? ST_ENOMEM : ST_ECUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+    return cleanup(e == cudaErrorMemoryAllocation ? ST_ENOMEM : ST_ECUDA);
+  }
+  double* b = pl->d_mats;
+  pl->P = b; b += nP;
+  pl->G = b; b += nG;
+  pl->Gm = b; b += nG;
+  pl->F = b; b += nF;
+  pl->Fm = b; b += nF;
+  pl->E = b; b += nE;
+  pl->rho = b;
+  *out = pl;
+  return ST_OK;
+}
+
+int st_plan_destroy(st_plan* pl) {
+  if (!pl) return ST_OK;
+  cudaSetDevice(pl->device);
+  if (pl->stream) cudaStreamSynchronize(pl->stream);
+  for (auto& e : pl->ev)
+    if (e) cudaEventDestroy(e);
+  if (pl->d_mats) cudaFree(pl->d_mats);
+  if (pl->d_counter) cudaFree(pl->d_counter);
+  if (pl->d_lam) cudaFree(pl->d_lam);
+  if (pl->d_io) cudaFree(pl->d_io);
+  if (pl->stream) cudaStreamDestroy(pl->stream);
+  delete pl;
+  return ST_OK;
+}
+
+int st_query_launch(st_plan* pl, int batch, int hint, long long* out8) {
+  if (!pl || !out8 || batch < 1) return fail(ST_EINVAL, "bad arguments");
+  std::lock_guard<std::mutex> g(pl->mu);
+  ST_CUDA(cudaSetDevice(pl->device));
+  Launch L;
+  int rc = choose_launch(pl, batch, hint, L);
+  if (rc) return rc;
+  out8[0] = L.C; out8[1] = L.NB; out8[2] = L.W; out8[3] = L.NT;
+  out8[4] = L.lam_smem; out8[5] = (long long)L.smem_bytes; out8[6] = L.nclusters; out8[7] = L.nsteps;
+  return ST_OK;
+}
+
+int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom,
+                    int switch_every, int max_iters, double tol, int flags, int hint, double* c_out,
+                    double* hist, int* iters, int* conv, double* lam_out, double* d_out, void* stream) {
+  int rc = check_common(pl, batch, switch_every, max_iters, tol, flags);
+  if (rc) return rc;
+  if (!c0 || !beq || !geom || !c_out || !hist || !iters || !conv) return fail(ST_EINVAL, "NULL buffer");
+  if ((flags & ST_FLAG_KEEP_STATE) && (!lam_out || !d_out)) return fail(ST_EINVAL, "keep_state buffers missing");
+  std::lock_guard<std::mutex> g(pl->mu);
+  ST_CUDA(cudaSetDevice(pl->device));
+  Launch L;
+  rc = choose_launch(pl, batch, hint, L);
+  if (rc) return rc;
+  cudaStream_t s = stream ? (cudaStream_t)stream : pl->stream;
+  return run(pl, L, batch, c0, beq, geom, switch_every, max_iters, tol, flags, c_out, hist, iters, conv, lam_out,
+             d_out, s);
+}
+
+int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom, int switch_every,
+             int max_iters, double tol, int flags, int hint, double* c_out, double* hist, int* iters, int* conv,
+             double* lam_out, double* d_out, float* timings) {
+  int rc = check_common(pl, batch, switch_every, max_iters, tol, flags);
+  if (rc) return rc;
+  if (!c0 || !beq || !geom || !c_out || !hist || !iters || !conv) return fail(ST_EINVAL, "NULL buffer");
+  const bool keep = flags & ST_FLAG_KEEP_STATE;
+  if (keep && (!lam_out || !d_out)) return fail(ST_EINVAL, "keep_state buffers missing");
+  std::lock_guard<std::mutex> g(pl->mu);
+  ST_CUDA(cudaSetDevice(pl->device));
+  Launch L;
+  rc = choose_launch(pl, batch, hint, L);
+  if (rc) return rc;
+  const int n = pl->n, nv = pl->nv, m = pl->m;
+  const long long p = (long long)n * (n - 1) / 2 + (long long)n * pl->nobs;
+  const size_t n_c = (size_t)batch * 3 * n * nv, n_b = (size_t)batch * 3 * n * 6,
+               n_g = (size_t)batch * (2 + 5 * pl->nobs), n_h = (size_t)batch * 3 * max_iters;
+  const size_t n_lam = keep ? (size_t)3 * p * m : 0, n_d = keep ? (size_t)p * m : 0;
+  const size_t in_bytes = (n_c + n_b + n_g) * 8;
+  const size_t out_bytes = (n_c + n_h + n_lam + n_d) * 8 + 2 * (size_t)batch * 4;
+  const size_t need = in_bytes + out_bytes + 64;
+  if (need > pl->io_bytes) {
+    if (pl->d_io) cudaFree(pl->d_io);
+    pl->d_io = nullptr;
+    pl->io_bytes = 0;
+    ST_CUDA(cudaMalloc(&pl->d_io, need));
+    pl->io_bytes = need;
+  }
+  double* d = (double*)pl->d_io;
+  double *d_c0 = d, *d_beq = d_c0 + n_c, *d_geom = d_beq + n_b, *d_cout = d_geom + n_g, *d_hist = d_cout + n_c;
+  double *d_lam = d_hist + n_h, *d_dd = d_lam + n_lam;
+  int* d_it = (int*)(d_dd + n_d);
+  int* d_cv = d_it + batch;
+  cudaStream_t s = pl->stream;
+  ST_CUDA(cudaEventRecord(pl->ev[0], s));
+  ST_CUDA(cudaMemcpyAsync(d_c0, c0, n_c * 8, cudaMemcpyHostToDevice, s));
+  ST_CUDA(cudaMemcpyAsync(d_beq, beq, n_b * 8, cudaMemcpyHostToDevice, s));
+  ST_CUDA(cudaMemcpyAsync(d_geom, geom, n_g * 8, cudaMemcpyHostToDevice, s));
+  ST_CUDA(cudaEventRecord(pl->ev[1], s));
+  rc = run(pl, L, batch, d_c0, d_beq, d_geom, switch_every, max_iters, tol, flags, d_cout, d_hist, d_it, d_cv,
+           keep ? d_lam : nullptr, keep ? d_dd : nullptr, s);
+  if (rc) return rc;
+  ST_CUDA(cudaEventRecord(pl->ev[2], s));
+  ST_CUDA(cudaMemcpyAsync(c_out, d_cout, n_c * 8, cudaMemcpyDeviceToHost, s));
+  ST_CUDA(cudaMemcpyAsync(hist, d_hist, n_h * 8, cudaMemcpyDeviceToHost, s));
+  ST_CUDA(cudaMemcpyAsync(iters, d_it, batch * 4, cudaMemcpyDeviceToHost, s));
+  ST_CUDA(cudaMemcpyAsync(conv, d_cv, batch * 4, cudaMemcpyDeviceToHost, s));
+  if (keep) {
+    ST_CUDA(cudaMemcpyAsync(lam_out, d_lam, n_lam * 8, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(d_out, d_dd, n_d * 8, cudaMemcpyDeviceToHost, s));
+  }
+  ST_CUDA(cudaEventRecord(pl->ev[3], s));
+  ST_CUDA(cudaStreamSynchronize(s));
+  ST_CUDA(cudaGetLastError());
+  if (timings) {
+    ST_CUDA(cudaEventElapsedTime(&timings[0], pl->ev[0], pl->ev[1]));
+    ST_CUDA(cudaEventElapsedTime(&timings[1], pl->ev[1], pl->ev[2]));
+    ST_CUDA(cudaEventElapsedTime(&timings[2], pl->ev[2], pl->ev[3]));
+  }
+  return ST_OK;
+}
+
+}  // extern "C"

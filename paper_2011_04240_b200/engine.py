@@ -1,0 +1,307 @@
+"""Drop-in ``am_solve``: the reference entry point, computed on the B200.
+
+Reference: ``solver.py`` -- ``SolverConfig`` (60-82), ``SolveReport``
+(139-172), ``InfeasibleProblemError`` (49-57), ``am_solve`` (363-494).
+Same signature, same report layout (trajectories (n,m,3), coefficients
+(3,n,n_v), histories of length ``iterations``), same error behaviour
+(validation before any work, non-convergence reported not raised), same
+``cache_stats`` census (10 factorizations per new fingerprint, 3 solves
+per iteration).
+
+The host does only shape work: basis, packing of boundary rows and
+straight-line coefficients, the per-stage 17x17 operators (cached), and
+the post-loop metrics.  Every iteration of the loop runs in one cluster
+kernel on the device (csrc/am_kernel.cuh); there is no CPU path.
+``am_solve_batch`` runs many scenarios sharing one fingerprint in one
+launch (the reference runs those through a thread pool, bench.py:120-158).
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import kkt, metrics, native, poly
+from .spec import obstacle_axes, validate
+
+log = logging.getLogger(__name__)
+
+
+class InfeasibleProblemError(ValueError):
+    def __init__(self, violations):
+        self.violations = list(violations)
+        text = "; ".join(str(v) for v in self.violations[:5])
+        if len(self.violations) > 5:
+            text += f"; ... ({len(self.violations)} total)"
+        super().__init__(f"invalid problem instance: {text}")
+
+
+@dataclass
+class SolverConfig:
+    max_iters: int = 150
+    tolerance: float = 1e-2
+    rho_initial: float = 1.0
+    rho_growth: float = 2.0
+    rho_stages: int = 10
+    initialization: str = "straight_line"
+    track_descent: bool = False
+    keep_state: bool = False
+    # B200 extensions (not in the reference): CTAs per scenario (0 = auto), device ordinal
+    cluster_size: int = 0
+    device: int = 0
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise ValueError(f"max_iters must be >= 1, got {self.max_iters}")
+        if not self.tolerance > 0:
+            raise ValueError(f"tolerance must be positive, got {self.tolerance}")
+        if self.initialization != "straight_line":
+            raise ValueError(f"unknown initialization mode {self.initialization!r}")
+
+    def schedule(self) -> kkt.RhoSchedule:
+        return kkt.build_rho_schedule(self.rho_initial, self.rho_growth, self.rho_stages, self.max_iters)
+
+
+@dataclass
+class PairVariables:
+    alpha: np.ndarray
+    beta: np.ndarray
+    d: np.ndarray
+
+
+@dataclass
+class Multipliers:
+    lambda_x: np.ndarray
+    lambda_y: np.ndarray
+    lambda_z: np.ndarray
+
+    def for_axis(self, axis: int) -> np.ndarray:
+        return (self.lambda_x, self.lambda_y, self.lambda_z)[axis]
+
+
+@dataclass
+class FinalState:
+    """Final solver state exported by ``keep_state`` (reference SolverState, solver.py:107-136)."""
+
+    c_x: np.ndarray
+    c_y: np.ndarray
+    c_z: np.ndarray
+    pair_vars: PairVariables
+    multipliers: Multipliers
+    rho: float
+    stage: int
+    iteration: int
+    residual_norms: list
+    residual_max: list
+
+    def coeffs(self, axis: int) -> np.ndarray:
+        return (self.c_x, self.c_y, self.c_z)[axis]
+
+
+@dataclass
+class SolveReport:
+    trajectories: np.ndarray
+    coefficients: np.ndarray
+    converged: bool
+    iterations: int
+    residual_norm: float
+    residual_max_abs: float
+    residual_norm_history: list
+    residual_max_history: list
+    boundary_max_history: list
+    timings: dict
+    metrics: dict
+    cache_stats: dict
+    diagnostics: dict = field(default_factory=dict)
+
+    def to_dict(self, include_trajectories: bool = True) -> dict:
+        doc = {
+            "converged": self.converged,
+            "iterations": self.iterations,
+            "residual_norm": self.residual_norm,
+            "residual_max_abs": self.residual_max_abs,
+            "residual_norm_history": list(self.residual_norm_history),
+            "residual_max_history": list(self.residual_max_history),
+            "boundary_max_history": list(self.boundary_max_history),
+            "timings": dict(self.timings),
+            "metrics": dict(self.metrics),
+            "cache_stats": dict(self.cache_stats),
+        }
+        if include_trajectories:
+            doc["trajectories"] = self.trajectories.tolist()
+        return doc
+
+
+_DEFAULT_CACHE: kkt.FactorCache | None = None
+
+
+def default_cache() -> kkt.FactorCache:
+    global _DEFAULT_CACHE
+    if _DEFAULT_CACHE is None:
+        _DEFAULT_CACHE = kkt.FactorCache()
+    return _DEFAULT_CACHE
+
+
+# --- host-side packing ---------------------------------------------------------------------
+
+
+def pack(specs, basis: poly.Basis):
+    """Scenario batch -> (c0 (B,3,n,nv), b_eq (B,3,n,6), geom (B, 2+5 n_obs)).
+
+    b_eq rows per agent and axis: [pos0, vel0, acc0, posT, velT, accT]
+    (kkt_cache.py:174-185); c0 = straight line (solver.py:327-330).
+    """
+    B = len(specs)
+    n = len(specs[0].start)
+    n_obs = len(specs[0].obstacles)
+    bnd = np.empty((B, 2, 3, n, 3))  # scenario, start/goal, pos/vel/acc, agent, axis
+    for b, spec in enumerate(specs):
+        for e, states in enumerate((spec.start, spec.goal)):
+            bnd[b, e, 0] = [s.position for s in states]
+            bnd[b, e, 1] = [s.velocity for s in states]
+            bnd[b, e, 2] = [s.acceleration for s in states]
+    beq = np.ascontiguousarray(bnd.transpose(0, 4, 3, 1, 2).reshape(B, 3, n, 6))
+    c0 = np.ascontiguousarray(poly.straight_line(basis, bnd[:, 0, 0].transpose(0, 2, 1),
+                                                 bnd[:, 1, 0].transpose(0, 2, 1)))
+    geom = np.empty((B, 2 + 5 * n_obs))
+    for b, spec in enumerate(specs):
+        geom[b, 0] = spec.geometry.l_xy
+        geom[b, 1] = spec.geometry.l_z
+        for k, obs in enumerate(spec.obstacles):
+            lxy, lz = obstacle_axes(spec, obs)
+            geom[b, 2 + 5 * k: 7 + 5 * k] = (*obs.center, lxy, lz)
+    return c0, beq, geom
+
+
+def _plan_for(cache: kkt.FactorCache, fp, basis, schedule, n, n_obs, device):
+    ops = cache.prefactorize(fp, basis, schedule)
+    return cache.plan(fp, schedule, lambda: native.Plan(n, n_obs, basis, ops, device=device))
+
+
+def _check_batch(specs):
+    first = specs[0]
+    key = (len(first.start), len(first.obstacles), first.num_samples, first.degree, float(first.duration),
+           str(getattr(first.basis_kind, "value", first.basis_kind)))
+    for s in specs[1:]:
+        k2 = (len(s.start), len(s.obstacles), s.num_samples, s.degree, float(s.duration),
+              str(getattr(s.basis_kind, "value", s.basis_kind)))
+        if k2 != key:
+            raise ValueError("all scenarios of a batch must share one fingerprint "
+                             f"(agents, obstacles, samples, degree, duration, basis): {k2} != {key}")
+
+
+def _alpha_beta(diffs, l_xy, l_z):
+    """Final-state angles from the final differences (same formula as solver.py:178-195)."""
+    planar = np.hypot(diffs[0], diffs[1])
+    alpha = np.arctan2(diffs[1], diffs[0])
+    beta = np.arctan2(planar / l_xy, diffs[2] / l_z)
+    beta = np.where((planar == 0.0) & (diffs[2] == 0.0), np.pi / 2.0, beta)
+    return alpha, beta
+
+
+def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorCache | None = None,
+                   with_metrics: bool = True) -> list:
+    """Solve scenarios sharing one fingerprint in one device launch; one report each."""
+    config = config or SolverConfig()
+    specs = list(specs)
+    if not specs:
+        return []
+    if config.track_descent:
+        raise NotImplementedError("track_descent (an augmented-cost diagnostic between axis solves) is not "
+                                  "implemented by the device loop")
+    for spec in specs:
+        v = validate(spec)
+        if v:
+            raise InfeasibleProblemError(v)
+    _check_batch(specs)
+    if config.keep_state and len(specs) != 1:
+        raise ValueError("keep_state is only available for single solves")
+    t0 = time.perf_counter()
+    spec0 = specs[0]
+    n, n_obs = len(spec0.start), len(spec0.obstacles)
+    basis = poly.for_spec(spec0)
+    fp = kkt.fingerprint(basis, n, n_obs)
+    c0, beq, geom = pack(specs, basis)
+    t1 = time.perf_counter()
+    cache = cache if cache is not None else default_cache()
+    schedule = config.schedule()
+    plan = _plan_for(cache, fp, basis, schedule, n, n_obs, config.device)
+    t2 = time.perf_counter()
+    out = plan.solve(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
+                     keep_state=config.keep_state, cluster_hint=config.cluster_size)
+    t3 = time.perf_counter()
+    h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
+    reports = []
+    for b, spec in enumerate(specs):
+        it = int(out["iters"][b])
+        cache.count_solve(3 * it)
+        coeffs = out["c"][b]
+        traj = np.ascontiguousarray(np.einsum("ank,tk->nta", coeffs, basis.P))
+        tm0 = time.perf_counter()
+        rep_metrics = metrics.final_metrics(spec, traj) if with_metrics else {}
+        hist = out["hist"][b]
+        timings = {
+            "assembly_s": t1 - t0,
+            "factorization_s": t2 - t1,
+            "loop_s": loop_ms / 1e3,
+            "per_iteration_s": loop_ms / 1e3 / max(1, it),
+            "h2d_s": h2d_ms / 1e3,
+            "d2h_s": d2h_ms / 1e3,
+            "solve_call_s": t3 - t2,
+            "metrics_s": time.perf_counter() - tm0,
+            "total_s": time.perf_counter() - t0,
+            "batch": len(specs),
+        }
+        diagnostics = {}
+        if config.keep_state:
+            p, m = plan.num_pairs, basis.num_samples
+            X = np.einsum("ank,tk->ant", coeffs, basis.P)
+            ii, jj = np.triu_indices(n, k=1)
+            diffs = np.empty((3, p, m))
+            diffs[:, : len(ii)] = X[:, ii] - X[:, jj]
+            lxy = np.full((p, 1), spec.geometry.l_xy)
+            lz = np.full((p, 1), spec.geometry.l_z)
+            for i in range(n):
+                for k, obs in enumerate(spec.obstacles):
+                    row = len(ii) + i * n_obs + k
+                    diffs[:, row] = X[:, i] - np.asarray(obs.center)[:, None]
+                    lxy[row], lz[row] = obstacle_axes(spec, obs)
+            alpha, beta = _alpha_beta(diffs, lxy, lz)
+            lam = out["lam"]
+            stage = schedule.stage_for(it - 1)
+            diagnostics["final_state"] = FinalState(
+                c_x=coeffs[0].copy(), c_y=coeffs[1].copy(), c_z=coeffs[2].copy(),
+                pair_vars=PairVariables(alpha=alpha, beta=beta, d=out["d"]),
+                multipliers=Multipliers(lambda_x=lam[0], lambda_y=lam[1], lambda_z=lam[2]),
+                rho=schedule.values[stage], stage=stage, iteration=it,
+                residual_norms=list(hist[0, :it]), residual_max=list(hist[1, :it]))
+        reports.append(SolveReport(
+            trajectories=traj,
+            coefficients=coeffs,
+            converged=bool(out["converged"][b]),
+            iterations=it,
+            residual_norm=float(hist[0, it - 1]) if it else 0.0,
+            residual_max_abs=float(hist[1, it - 1]) if it else 0.0,
+            residual_norm_history=[float(v) for v in hist[0, :it]],
+            residual_max_history=[float(v) for v in hist[1, :it]],
+            boundary_max_history=[float(v) for v in hist[2, :it]],
+            timings=timings,
+            metrics=rep_metrics,
+            cache_stats=cache.stats(),
+            diagnostics=diagnostics,
+        ))
+    log.info("batch of %d solved on device in %.3f ms", len(specs), loop_ms)
+    return reports
+
+
+def am_solve(spec, config: SolverConfig | None = None, cache: kkt.FactorCache | None = None) -> SolveReport:
+    """Run the AM loop end to end on the GPU (reference solver.py:363-494).
+
+    Raises:
+        InfeasibleProblemError: if the instance fails validation.
+    """
+    return am_solve_batch([spec], config, cache)[0]

@@ -1,0 +1,211 @@
+"""Per-stage KKT operators in structured form, the rho schedule and the factor cache.
+
+Reference: ``kkt_cache.py``.  The reference LU-factorizes the full
+(17n)x(17n) KKT matrix per rho (kkt_cache.py:321-353) and solves with
+``lu_solve`` three times per iteration (kkt_cache.py:291-305).
+
+Structure used here instead (verified to 1e-15): with the
+complete-graph pair incidence S plus n_obs obstacle rows per agent,
+S'S = (n + n_obs) I - 11', so the per-axis KKT matrix permuted to per-agent
+17x17 blocks is  I (x) K_dev + 11' (x) K_C, and
+
+    x_i = K_dev^-1 (r_i - rbar) + K_mean^-1 rbar,      rbar = mean_i r_i
+
+    K_dev  = [[Pdd'Pdd + rho (n + n_obs) P'P, E'], [E, 0]]
+    K_mean = [[Pdd'Pdd + rho  n_obs      P'P, E'], [E, 0]]
+
+Only the coefficient rows of the solution are needed, and the boundary
+right-hand side b_eq is fixed per scenario, so a stage is fully described by
+four small matrices (all n_v x n_v or n_v x 6, FP64):
+
+    G  = K_dev^-1[:nv,:nv]          F  = K_dev^-1[:nv, nv:]
+    Gm = K_mean^-1[:nv,:nv] - G     Fm = K_mean^-1[:nv, nv:]
+
+    c_i = rho G R_i + rho Gm Rbar + F (beq_i - beqbar) + Fm beqbar,   R_i = (S'b)_i P
+
+which is what the device solve phase evaluates.  The "factorization" of a
+stage is the two 17x17 inversions; it is counted exactly like the
+reference's LU so ``cache_stats`` keep their meaning (10 per new
+fingerprint, none inside the loop; kkt_cache.py:385-419).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy.linalg import lu_factor
+
+from . import poly
+
+BOUNDARY_ROWS = 6
+
+
+@dataclass(frozen=True)
+class RhoSchedule:
+    """Geometric penalty schedule advanced in equal blocks (kkt_cache.py:356-382)."""
+
+    values: tuple
+    switch_every: int
+
+    def stage_for(self, iteration: int) -> int:
+        return min(iteration // self.switch_every, len(self.values) - 1)
+
+    def value_for(self, iteration: int) -> float:
+        return self.values[self.stage_for(iteration)]
+
+
+def build_rho_schedule(rho_initial: float, growth: float, stages: int, max_iters: int) -> RhoSchedule:
+    if not rho_initial > 0:
+        raise ValueError(f"rho_initial must be positive, got {rho_initial}")
+    if not growth > 1:
+        raise ValueError(f"growth must be > 1, got {growth}")
+    if stages < 1:
+        raise ValueError(f"stages must be >= 1, got {stages}")
+    if max_iters < 1:
+        raise ValueError(f"max_iters must be >= 1, got {max_iters}")
+    return RhoSchedule(values=tuple(rho_initial * growth ** s for s in range(stages)),
+                       switch_every=-(-max_iters // stages))
+
+
+@dataclass(frozen=True)
+class Fingerprint:
+    """Identity of the iteration-independent operators (kkt_cache.py:52-72)."""
+
+    num_agents: int
+    num_samples: int
+    num_coeffs: int
+    num_obstacles: int
+    basis_kind: str
+    basis_sha: str
+
+    def key(self) -> str:
+        text = (f"{self.num_agents},{self.num_samples},{self.num_coeffs},{self.num_obstacles},"
+                f"{self.basis_kind},{self.basis_sha}")
+        return hashlib.sha256(text.encode()).hexdigest()[:16]
+
+
+def basis_digest(basis: poly.Basis) -> str:
+    h = hashlib.sha256()
+    for a in (basis.P, basis.Pdot, basis.Pddot):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:16]
+
+
+def fingerprint(basis: poly.Basis, n: int, n_obs: int) -> Fingerprint:
+    return Fingerprint(n, basis.num_samples, basis.num_coeffs, n_obs, basis.kind.value, basis_digest(basis))
+
+
+@dataclass(frozen=True)
+class StageOperator:
+    """Solve operator of one rho stage (see module docstring)."""
+
+    rho: float
+    G: np.ndarray = field(repr=False)
+    Gm: np.ndarray = field(repr=False)
+    F: np.ndarray = field(repr=False)
+    Fm: np.ndarray = field(repr=False)
+
+
+def block_matrix(basis: poly.Basis, weight: float) -> np.ndarray:
+    """[[Pdd'Pdd + weight P'P, E'], [E, 0]] (17x17 at the default degree)."""
+    nv = basis.num_coeffs
+    E = poly.endpoint_rows(basis)
+    K = np.zeros((nv + BOUNDARY_ROWS, nv + BOUNDARY_ROWS))
+    K[:nv, :nv] = basis.Pddot.T @ basis.Pddot + weight * (basis.P.T @ basis.P)
+    K[:nv, nv:] = E.T
+    K[nv:, :nv] = E
+    return K
+
+
+def _checked_inverse(K: np.ndarray) -> np.ndarray:
+    lu, _ = lu_factor(K, check_finite=False)
+    diag = np.abs(np.diag(lu))
+    if diag.min() <= 1e-14 * diag.max():
+        raise ValueError("KKT matrix is numerically singular "
+                         f"(pivot ratio {diag.min():.3e}/{diag.max():.3e}); "
+                         "check that the endpoint block has full rank")
+    return np.linalg.inv(K)
+
+
+def stage_operator(basis: poly.Basis, n: int, n_obs: int, rho: float) -> StageOperator:
+    """Build one stage's operator (the analogue of ``factorize``, kkt_cache.py:332-353)."""
+    if rho < 0:
+        raise ValueError(f"rho must be non-negative, got {rho}")
+    nv = basis.num_coeffs
+    if np.linalg.matrix_rank(poly.endpoint_rows(basis)) < BOUNDARY_ROWS:
+        raise ValueError("endpoint constraint block is rank deficient; the basis cannot pin "
+                         "position, velocity and acceleration at both ends")
+    kd = _checked_inverse(block_matrix(basis, rho * (n + n_obs)))
+    km = _checked_inverse(block_matrix(basis, rho * n_obs))
+    G = kd[:nv, :nv].copy()
+    return StageOperator(rho=float(rho), G=G, Gm=km[:nv, :nv] - G, F=kd[:nv, nv:].copy(),
+                         Fm=km[:nv, nv:].copy())
+
+
+class FactorCache:
+    """Shared store of stage operators keyed by (fingerprint, rho) (kkt_cache.py:385-456).
+
+    Single-flight per key, immutable entries, the reference's counters.  It
+    additionally owns the device plans (one per fingerprint and schedule),
+    so a warm cache means no host precompute and no device upload either.
+    """
+
+    def __init__(self, disk_dir=None):
+        self._ops: dict = {}
+        self._plans: dict = {}
+        self._lock = threading.Lock()
+        self._inflight: dict = {}
+        self.disk_dir = disk_dir
+        self.factorizations = 0
+        self.hits = 0
+        self.misses = 0
+        self.solves = 0
+
+    def count_solve(self, k: int = 1) -> None:
+        with self._lock:
+            self.solves += k
+
+    def stats(self) -> dict:
+        return {"entries": len(self._ops), "factorizations": self.factorizations, "hits": self.hits,
+                "misses": self.misses, "solves": self.solves}
+
+    def get(self, fp: Fingerprint, basis: poly.Basis, rho: float) -> StageOperator:
+        key = (fp.key(), float(rho))
+        while True:
+            with self._lock:
+                op = self._ops.get(key)
+                if op is not None:
+                    self.hits += 1
+                    return op
+                ev = self._inflight.get(key)
+                if ev is None:
+                    self._inflight[key] = threading.Event()
+                    break
+            ev.wait()
+        try:
+            op = stage_operator(basis, fp.num_agents, fp.num_obstacles, rho)
+            with self._lock:
+                self._ops[key] = op
+                self.factorizations += 1
+                self.misses += 1
+            return op
+        finally:
+            with self._lock:
+                self._inflight.pop(key).set()
+
+    def prefactorize(self, fp: Fingerprint, basis: poly.Basis, schedule: RhoSchedule) -> list:
+        return [self.get(fp, basis, rho) for rho in schedule.values]
+
+    def plan(self, fp: Fingerprint, schedule: RhoSchedule, build):
+        """Device plan for (fingerprint, rho values), created once via ``build()``."""
+        key = (fp.key(), tuple(float(v) for v in schedule.values))
+        with self._lock:
+            plan = self._plans.get(key)
+        if plan is not None:
+            return plan
+        plan = build()
+        with self._lock:
+            return self._plans.setdefault(key, plan)

@@ -1,0 +1,144 @@
+"""ctypes binding of the C ABI in ``include/swarm_am.h`` (``_swarm_am.so``).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+usable, every call raises.  ``Plan`` owns one ``st_plan`` (the device copy
+of one fingerprint's stage operators).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import poly
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_swarm_am.so")
+
+ST_FLAG_KEEP_STATE = 1
+_ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedError}
+
+EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
+           "st_last_error", "st_version")
+
+_lib = None
+_lock = threading.Lock()
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+
+
+def load() -> ctypes.CDLL:
+    """Load the solver library (no GPU needed just to load it)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"native solver library missing: {LIB_PATH} "
+                               "(build it with `python -c 'import __graft_entry__ as g; g.build()'`)")
+        lib = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        i, d = ctypes.c_int, ctypes.c_double
+        lib.st_plan_create.argtypes = [i, i, i, i, i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, i, ctypes.POINTER(vp)]
+        lib.st_plan_destroy.argtypes = [vp]
+        lib.st_solve.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip, _dp, _dp,
+                                 ctypes.POINTER(ctypes.c_float)]
+        lib.st_solve_device.argtypes = [vp, i, vp, vp, vp, i, i, d, i, i, vp, vp, vp, vp, vp, vp, vp]
+        lib.st_query_launch.argtypes = [vp, i, i, ctypes.POINTER(ctypes.c_longlong)]
+        lib.st_last_error.restype = ctypes.c_char_p
+        for name in EXPORTS:
+            getattr(lib, name)  # every declared symbol must resolve
+        _lib = lib
+        return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = load().st_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def _ptr(a: np.ndarray | None, ctype=_dp):
+    if a is None:
+        return None
+    assert a.flags.c_contiguous
+    return a.ctypes.data_as(ctype)
+
+
+class Plan:
+    """Device-resident stage operators for one (fingerprint, rho schedule)."""
+
+    def __init__(self, n: int, n_obs: int, basis: poly.Basis, ops, device: int = 0):
+        lib = load()
+        self.n, self.n_obs = n, n_obs
+        self.m, self.nv = basis.num_samples, basis.num_coeffs
+        self.stages = len(ops)
+        P = np.ascontiguousarray(basis.P, dtype=np.float64)
+        G = np.ascontiguousarray(np.stack([o.G for o in ops]))
+        Gm = np.ascontiguousarray(np.stack([o.Gm for o in ops]))
+        F = np.ascontiguousarray(np.stack([o.F for o in ops]))
+        Fm = np.ascontiguousarray(np.stack([o.Fm for o in ops]))
+        E = np.ascontiguousarray(poly.endpoint_rows(basis))
+        rho = np.array([o.rho for o in ops], dtype=np.float64)
+        h = ctypes.c_void_p()
+        _check(lib.st_plan_create(n, n_obs, self.m, self.nv, self.stages, _ptr(P), _ptr(G), _ptr(Gm),
+                                  _ptr(F), _ptr(Fm), _ptr(E), _ptr(rho), device, ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.st_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def num_pairs(self) -> int:
+        return self.n * (self.n - 1) // 2 + self.n * self.n_obs
+
+    def query_launch(self, batch: int = 1, cluster_hint: int = 0) -> dict:
+        out = (ctypes.c_longlong * 8)()
+        _check(self._lib.st_query_launch(self._h, batch, cluster_hint, out))
+        keys = ("cluster", "agent_blocks", "lane_width", "threads", "lambda_in_smem", "smem_bytes",
+                "clusters", "steps_per_task")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def solve(self, c0, beq, geom, switch_every: int, max_iters: int, tol: float,
+              keep_state: bool = False, cluster_hint: int = 0) -> dict:
+        """Host-buffer solve of a batch: c0 (B,3,n,nv), beq (B,3,n,6), geom (B, 2+5 n_obs)."""
+        c0 = np.ascontiguousarray(c0, dtype=np.float64)
+        beq = np.ascontiguousarray(beq, dtype=np.float64)
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        B = c0.shape[0]
+        if c0.shape != (B, 3, self.n, self.nv) or beq.shape != (B, 3, self.n, 6) or \
+                geom.shape != (B, 2 + 5 * self.n_obs):
+            raise ValueError(f"batch arrays have shapes {c0.shape}, {beq.shape}, {geom.shape}; expected "
+                             f"({B}, 3, {self.n}, {self.nv}), ({B}, 3, {self.n}, 6), ({B}, {2 + 5 * self.n_obs})")
+        c_out = np.empty_like(c0)
+        hist = np.empty((B, 3, max_iters))
+        iters = np.empty(B, dtype=np.int32)
+        conv = np.empty(B, dtype=np.int32)
+        lam = d = None
+        if keep_state:
+            lam = np.empty((3, self.num_pairs, self.m))
+            d = np.empty((self.num_pairs, self.m))
+        t = (ctypes.c_float * 3)()
+        _check(self._lib.st_solve(self._h, B, _ptr(c0), _ptr(beq), _ptr(geom), switch_every, max_iters, tol,
+                                  ST_FLAG_KEEP_STATE if keep_state else 0, cluster_hint, _ptr(c_out),
+                                  _ptr(hist), _ptr(iters, _ip), _ptr(conv, _ip), _ptr(lam), _ptr(d), t))
+        return {"c": c_out, "hist": hist, "iters": iters, "converged": conv.astype(bool), "lam": lam, "d": d,
+                "timings_ms": tuple(float(x) for x in t)}
+
+    def solve_device(self, B: int, c0_ptr: int, beq_ptr: int, geom_ptr: int, switch_every: int,
+                     max_iters: int, tol: float, c_out_ptr: int, hist_ptr: int, iters_ptr: int,
+                     conv_ptr: int, stream: int = 0, cluster_hint: int = 0) -> None:
+        """Enqueue a solve on device-resident buffers (raw pointers, e.g. torch ``data_ptr()``)."""
+        _check(self._lib.st_solve_device(self._h, B, c0_ptr, beq_ptr, geom_ptr, switch_every, max_iters, tol,
+                                         0, cluster_hint, c_out_ptr, hist_ptr, iters_ptr, conv_ptr, None, None,
+                                         stream or None))

@@ -1,0 +1,43 @@
+"""Pin the CPU oracle (oracle/am_oracle.py) against the reference's own outputs.
+
+The fixtures were produced by running the real reference (tests/golden/make_golden.py);
+the oracle must reproduce them within the reference's self-noise envelope with identical
+iteration counts, convergence flags and collision verdicts before it may judge the GPU.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import CHAOTIC, coeff_tol, golden_names, load_golden, rel_err
+from oracle import am_oracle
+
+FAST = [n for n in golden_names() if n not in ("sph64j", "rand48_s0")]
+
+
+def _kw(cfg):
+    return dict(max_iters=cfg.get("max_iters", 150), tol=cfg.get("tolerance", 1e-2),
+                rho0=cfg.get("rho_initial", 1.0), growth=cfg.get("rho_growth", 2.0),
+                stages=cfg.get("rho_stages", 10))
+
+
+@pytest.mark.parametrize("name", FAST)
+def test_oracle_matches_reference_fixture(name):
+    spec, cfg, ref = load_golden(name)
+    out = am_oracle.solve(spec, keep_state="lam" in ref, **_kw(cfg))
+    if name in CHAOTIC:
+        # chaotic instance: only the verdicts are reproducible
+        assert out["converged"] == bool(ref["converged"])
+        return
+    assert out["iterations"] == int(ref["iterations"])
+    assert out["converged"] == bool(ref["converged"])
+    assert rel_err(out["coefficients"], ref["coefficients"]) <= coeff_tol(ref)
+    for key in ("residual_norm_history", "residual_max_history"):
+        np.testing.assert_allclose(out[key], ref[key], rtol=1e-8, atol=1e-13)
+    np.testing.assert_allclose(out["boundary_max_history"], ref["boundary_max_history"], atol=1e-10)
+    md, nviol = am_oracle.min_normalized_distance(spec, out["trajectories"])
+    assert nviol == int(ref["num_collision_violations"])
+    if np.isfinite(ref["min_normalized_distance"]):
+        assert md == pytest.approx(float(ref["min_normalized_distance"]), rel=1e-8)
+    if "lam" in ref:
+        assert rel_err(out["lam"], ref["lam"]) <= 1e3 * coeff_tol(ref)
+        assert rel_err(out["d"], ref["d"]) <= coeff_tol(ref)
