@@ -105,6 +105,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_c, 3LL * n * nv);
   take(k.o_X, 3LL * L.tmax * NP);
   take(k.o_q, 3LL * L.tmax * NP);
+  take(k.o_qs, 3LL * L.tmax);
   take(k.o_P, (long long)L.tmax * nv);
   take(k.o_r1, (long long)C * L.own_max * 3 * nv);
   take(k.o_rS, (long long)C * 3 * nv);
