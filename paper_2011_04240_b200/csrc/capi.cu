@@ -33,18 +33,19 @@ int fail(int code, const std::string& msg) {
 using KernelFn = void (*)(swarm::KParams);
 
 struct KernelEntry {
-  int NB, NT;
+  int NB, NT, NVMAX;
   KernelFn fn;
 };
 
 const KernelEntry kKernels[] = {
-    {1, 512, swarm::am_cluster_kernel<1, 512>},
-    {2, 512, swarm::am_cluster_kernel<2, 512>},
-    {4, 256, swarm::am_cluster_kernel<4, 256>},
-    {8, 256, swarm::am_cluster_kernel<8, 256>},
+    {1, 512, 12, swarm::am_cluster_kernel<1, 512, 12>}, {2, 512, 12, swarm::am_cluster_kernel<2, 512, 12>},
+    {4, 256, 12, swarm::am_cluster_kernel<4, 256, 12>}, {8, 256, 12, swarm::am_cluster_kernel<8, 256, 12>},
+    {1, 512, 16, swarm::am_cluster_kernel<1, 512, 16>}, {2, 512, 16, swarm::am_cluster_kernel<2, 512, 16>},
+    {4, 256, 16, swarm::am_cluster_kernel<4, 256, 16>}, {8, 256, 16, swarm::am_cluster_kernel<8, 256, 16>},
 };
 
 struct Launch {
+  int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
   int lam_smem = 0, nclusters = 0;
   size_t smem_bytes = 0;
@@ -56,7 +57,7 @@ struct Launch {
 }  // namespace
 
 struct st_plan {
-  int n, nobs, m, nv, S, device;
+  int n, nobs, m, nv, S, device, nvmax;
   double* d_mats = nullptr;  // P | G | Gm | F | Fm | E | rho
   const double *P, *G, *Gm, *F, *Fm, *E, *rho;
   cudaStream_t stream = nullptr;
@@ -92,7 +93,7 @@ int count_steps(int n, int nobs, int NB) {
 // Shared-memory carve-up for cluster size C; returns total doubles (lambda excluded).
 long long layout(st_plan* pl, Launch& L, int C) {
   swarm::KParams& k = L.kp;
-  const int NP = L.NB * 32, nv = pl->nv, n = pl->n;
+  const int NP = L.NB * 32, n = pl->n;
   L.C = C;
   L.tmax = ceil_div(pl->m, C);
   L.tasks_max = ceil_div(L.tmax, 32 / L.W);
@@ -102,20 +103,19 @@ long long layout(st_plan* pl, Launch& L, int C) {
     off = (int)o;
     o += (cnt + 1) & ~1LL;  // keep 16-byte alignment
   };
-  take(k.o_c, 3LL * n * nv);
-  take(k.o_X, 3LL * L.tmax * NP);
+  const int NV = L.NVMAX;
+  take(k.o_c, 3LL * n * NV);
   take(k.o_q, 3LL * L.tmax * NP);
   take(k.o_qs, 3LL * L.tmax);
-  take(k.o_P, (long long)L.tmax * nv);
-  take(k.o_r1, (long long)C * L.own_max * 3 * nv);
-  take(k.o_rS, (long long)C * 3 * nv);
+  take(k.o_P, (long long)L.tmax * NV);
+  take(k.o_r1, (long long)C * L.own_max * 3 * NV);
+  take(k.o_rS, (long long)C * 3 * NV);
   take(k.o_rN, 2LL * C);
   take(k.o_rB, C);
-  take(k.o_R, (long long)L.own_max * 3 * nv);
-  take(k.o_Rb, 3LL * nv);
-  take(k.o_cl, (long long)L.own_max * 3 * nv);
-  take(k.o_gap, 18LL * L.own_max);
-  take(k.o_geo, 2 + 5LL * pl->nobs);
+  take(k.o_R, (long long)L.own_max * 3 * NV);
+  take(k.o_Rb, 3LL * NV);
+  take(k.o_cl, (long long)L.own_max * 3 * NV);
+  take(k.o_geo, 8 + 8LL * pl->nobs);
   take(k.o_beq, 18LL * L.own_max);
   take(k.o_bb, 18);
   take(k.o_wp, 2LL * (L.NT / 32));
@@ -128,13 +128,13 @@ long long layout(st_plan* pl, Launch& L, int C) {
 int choose_launch(st_plan* pl, int batch, int hint, Launch& L) {
   const int n = pl->n;
   if (n < 1 || n > 256) return fail(ST_EUNSUPPORTED, "n_agents must be in [1, 256] for the compiled kernels");
-  if (pl->nv > 16) return fail(ST_EUNSUPPORTED, "n_coeffs must be <= 16 (degree <= 15)");
   const int nb_need = n <= 32 ? 1 : ceil_div(n, 32);
   const KernelEntry* ke = nullptr;
   for (const auto& e : kKernels)
-    if (e.NB >= nb_need) { ke = &e; break; }
+    if (e.NVMAX == pl->nvmax && e.NB >= nb_need) { ke = &e; break; }
   if (!ke) return fail(ST_EUNSUPPORTED, "no kernel for this agent count");
   L.NB = ke->NB;
+  L.NVMAX = ke->NVMAX;
   L.NT = ke->NT;
   L.fn = ke->fn;
   if (L.NB == 1) {
@@ -261,6 +261,7 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
   *out = nullptr;
   if (n < 1 || nobs < 0 || m < 2 || nv < 6 || S < 1)
     return fail(ST_EINVAL, "bad dimensions (need n>=1, n_obs>=0, m>=2, nv>=6, stages>=1)");
+  if (nv > 16) return fail(ST_EUNSUPPORTED, "n_coeffs must be <= 16 (degree <= 15)");
   if (!P || !G || !Gm || !F || !Fm || !E || !rho) return fail(ST_EINVAL, "NULL operator pointer");
   int ndev = 0;
   ST_CUDA(cudaGetDeviceCount(&ndev));
@@ -268,15 +269,26 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
   ST_CUDA(cudaSetDevice(device));
   st_plan* pl = new st_plan();
   pl->n = n; pl->nobs = nobs; pl->m = m; pl->nv = nv; pl->S = S; pl->device = device;
-  const size_t nP = (size_t)m * nv, nG = (size_t)S * nv * nv, nF = (size_t)S * nv * 6, nE = 6 * (size_t)nv;
+  const int NV = nv <= 12 ? 12 : 16;
+  pl->nvmax = NV;
+  const size_t nP = (size_t)m * NV, nG = (size_t)S * NV * NV, nF = (size_t)S * NV * 6, nE = 6 * (size_t)NV;
   const size_t total = nP + 2 * nG + 2 * nF + nE + S;
-  std::vector<double> h(total);
+  std::vector<double> h(total, 0.0);
   size_t o = 0;
-  auto put = [&](const double* src, size_t cnt) {
-    std::memcpy(h.data() + o, src, cnt * sizeof(double));
-    o += cnt;
+  // copy a (count x rows x cols) block into a zero-padded (count x prow x pcol) one
+  auto put = [&](const double* src, int count, int rows, int cols, int prow, int pcol) {
+    for (int b = 0; b < count; ++b)
+      for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) h[o + ((size_t)b * prow + r) * pcol + c] = src[((size_t)b * rows + r) * cols + c];
+    o += (size_t)count * prow * pcol;
   };
-  put(P, nP); put(G, nG); put(Gm, nG); put(F, nF); put(Fm, nF); put(E, nE); put(rho, S);
+  put(P, 1, m, nv, m, NV);
+  put(G, S, nv, nv, NV, NV);
+  put(Gm, S, nv, nv, NV, NV);
+  put(F, S, nv, 6, NV, 6);
+  put(Fm, S, nv, 6, NV, 6);
+  put(E, 1, 6, nv, 6, NV);
+  put(rho, 1, 1, S, 1, S);
   auto cleanup = [&](int code) {
     if (pl->d_mats) cudaFree(pl->d_mats);
     if (pl->d_counter) cudaFree(pl->d_counter);
