@@ -33,21 +33,27 @@ int fail(int code, const std::string& msg) {
 using KernelFn = void (*)(swarm::KParams);
 
 struct KernelEntry {
-  int NB, NT, NVMAX;
+  int NB, NT, NVMAX, LAM;
   KernelFn fn;
 };
 
+using swarm::am_cluster_kernel;
+constexpr int kS = swarm::LAM_SMEM, kG = swarm::LAM_GLOBAL, kK = swarm::LAM_GLOBAL_KEEP;
+// lambda fits in shared memory only for n <= 32 (NB == 1); larger fleets stream it from L2.
 const KernelEntry kKernels[] = {
-    {1, 512, 12, swarm::am_cluster_kernel<1, 512, 12>}, {2, 512, 12, swarm::am_cluster_kernel<2, 512, 12>},
-    {4, 256, 12, swarm::am_cluster_kernel<4, 256, 12>}, {8, 256, 12, swarm::am_cluster_kernel<8, 256, 12>},
-    {1, 512, 16, swarm::am_cluster_kernel<1, 512, 16>}, {2, 512, 16, swarm::am_cluster_kernel<2, 512, 16>},
-    {4, 256, 16, swarm::am_cluster_kernel<4, 256, 16>}, {8, 256, 16, swarm::am_cluster_kernel<8, 256, 16>},
+    {1, 512, 12, kS, am_cluster_kernel<1, 512, 12, kS>}, {1, 512, 12, kG, am_cluster_kernel<1, 512, 12, kG>},
+    {1, 512, 12, kK, am_cluster_kernel<1, 512, 12, kK>}, {1, 512, 16, kS, am_cluster_kernel<1, 512, 16, kS>},
+    {1, 512, 16, kG, am_cluster_kernel<1, 512, 16, kG>}, {1, 512, 16, kK, am_cluster_kernel<1, 512, 16, kK>},
+    {2, 384, 12, kG, am_cluster_kernel<2, 384, 12, kG>}, {2, 384, 12, kK, am_cluster_kernel<2, 384, 12, kK>},
+    {2, 384, 16, kG, am_cluster_kernel<2, 384, 16, kG>}, {2, 384, 16, kK, am_cluster_kernel<2, 384, 16, kK>},
+    {4, 256, 12, kG, am_cluster_kernel<4, 256, 12, kG>}, {4, 256, 12, kK, am_cluster_kernel<4, 256, 12, kK>},
+    {8, 256, 12, kG, am_cluster_kernel<8, 256, 12, kG>}, {8, 256, 12, kK, am_cluster_kernel<8, 256, 12, kK>},
 };
 
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0;
+  int lam_smem = 0, nclusters = 0, qslots = 0;
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -93,10 +99,12 @@ int count_steps(int n, int nobs, int NB) {
 // Shared-memory carve-up for cluster size C; returns total doubles (lambda excluded).
 long long layout(st_plan* pl, Launch& L, int C) {
   swarm::KParams& k = L.kp;
-  const int NP = L.NB * 32, n = pl->n;
+  const int NP = L.NB * 32, n = pl->n, NW = L.NT / 32, TPW = 32 / L.W;
   L.C = C;
   L.tmax = ceil_div(pl->m, C);
-  L.tasks_max = ceil_div(L.tmax, 32 / L.W);
+  L.tasks_max = ceil_div(L.tmax, TPW);               // time groups of the largest CTA
+  const int spw = ceil_div(L.tasks_max * L.nsteps, NW);  // steps per warp (largest CTA)
+  L.qslots = ceil_div(spw, L.nsteps) + 1;            // groups a warp can touch
   L.own_max = ceil_div(n, C);
   long long o = 0;
   auto take = [&](int& off, long long cnt) {
@@ -105,8 +113,8 @@ long long layout(st_plan* pl, Launch& L, int C) {
   };
   const int NV = L.NVMAX;
   take(k.o_c, 3LL * n * NV);
-  take(k.o_q, 3LL * L.tmax * NP);
-  take(k.o_qs, 3LL * L.tmax);
+  take(k.o_qp, (long long)NW * L.qslots * 3 * NP);
+  take(k.o_qsp, (long long)NW * L.qslots * 3 * 32);
   take(k.o_P, (long long)L.tmax * NV);
   take(k.o_r1, (long long)C * L.own_max * 3 * NV);
   take(k.o_rS, (long long)C * 3 * NV);
@@ -118,55 +126,63 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_geo, 8 + 8LL * pl->nobs);
   take(k.o_beq, 18LL * L.own_max);
   take(k.o_bb, 18);
-  take(k.o_wp, 2LL * (L.NT / 32));
+  take(k.o_wp, 2LL * NW);
   take(k.o_misc, 2);
   k.o_lam = (int)o;
   L.lam_per_cta = (long long)L.tasks_max * L.nsteps * 96;
   return o;
 }
 
-int choose_launch(st_plan* pl, int batch, int hint, Launch& L) {
+const KernelEntry* find_kernel(int NB, int NVMAX, int LAM) {
+  for (const auto& e : kKernels)
+    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM) return &e;
+  return nullptr;
+}
+
+int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
   const int n = pl->n;
   if (n < 1 || n > 256) return fail(ST_EUNSUPPORTED, "n_agents must be in [1, 256] for the compiled kernels");
   const int nb_need = n <= 32 ? 1 : ceil_div(n, 32);
-  const KernelEntry* ke = nullptr;
-  for (const auto& e : kKernels)
-    if (e.NVMAX == pl->nvmax && e.NB >= nb_need) { ke = &e; break; }
-  if (!ke) return fail(ST_EUNSUPPORTED, "no kernel for this agent count");
-  L.NB = ke->NB;
-  L.NVMAX = ke->NVMAX;
-  L.NT = ke->NT;
-  L.fn = ke->fn;
-  if (L.NB == 1) {
+  int NB = 0;
+  for (int cand : {1, 2, 4, 8})
+    if (cand >= nb_need && find_kernel(cand, pl->nvmax, swarm::LAM_GLOBAL)) { NB = cand; break; }
+  if (!NB) return fail(ST_EUNSUPPORTED, "no compiled kernel for this agent count and basis degree");
+  L.NB = NB;
+  L.NVMAX = pl->nvmax;
+  if (NB == 1) {
     int w = 2;
     while (w < n) w <<= 1;
     L.W = w;
   } else {
     L.W = 32;
   }
-  L.nsteps = count_steps(n, pl->nobs, L.NB);
+  L.nsteps = count_steps(n, pl->nobs, NB);
   const long long budget = pl->smem_optin / 8;
-
-  ST_CUDA(cudaFuncSetAttribute(L.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   std::vector<int> cands;
   if (hint > 0) {
     cands.push_back(hint);
   } else if (batch == 1) {
-    cands = {16, 8, 4, 2, 1};
+    cands = {16, 8, 4, 2, 1};  // latency: spread one scenario widest
   } else {
-    cands = {1, 2, 4, 8, 16};
+    cands = {1, 2, 4, 8, 16};  // throughput: smallest cluster that keeps lambda on chip
   }
-  // pass 0: lambda in smem (throughput order: smallest C that fits; latency order: largest C)
+  // pass 0: lambda in shared memory; pass 1: lambda in a global (L2-resident) slab
   for (int pass = 0; pass < 2; ++pass) {
+    const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
+    if (keep && pass == 0) continue;
+    const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam);
+    if (!ke) continue;
     for (int C : cands) {
       if (C > pl->m || C < 1 || C > 16) continue;
       Launch T = L;
+      T.NT = ke->NT;
+      T.fn = ke->fn;
       const long long base = layout(pl, T, C);
-      const bool fits = base + T.lam_per_cta <= budget;
-      if (pass == 0 && !fits) continue;
-      if (base > budget) continue;
-      T.lam_smem = fits ? 1 : 0;
-      T.smem_bytes = (size_t)(base + (T.lam_smem ? T.lam_per_cta : 0)) * 8;
+      const long long need = base + (pass == 0 ? T.lam_per_cta : 0);
+      if (need > budget) continue;
+      T.lam_smem = pass == 0 ? 1 : 0;
+      T.smem_bytes = (size_t)need * 8;
+      ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_bytes));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(C);
@@ -201,7 +217,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.n = pl->n; k.nobs = pl->nobs; k.m = pl->m; k.nv = pl->nv; k.S = pl->S;
   k.P = pl->P; k.G = pl->G; k.Gm = pl->Gm; k.F = pl->F; k.Fm = pl->Fm; k.E = pl->E; k.rho = pl->rho;
   k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
-  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta;
+  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots;
   k.B = batch; k.gstride = 2 + 5 * pl->nobs;
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
@@ -338,7 +354,7 @@ int st_query_launch(st_plan* pl, int batch, int hint, long long* out8) {
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  int rc = choose_launch(pl, batch, hint, L);
+  int rc = choose_launch(pl, batch, hint, false, L);
   if (rc) return rc;
   out8[0] = L.C; out8[1] = L.NB; out8[2] = L.W; out8[3] = L.NT;
   out8[4] = L.lam_smem; out8[5] = (long long)L.smem_bytes; out8[6] = L.nclusters; out8[7] = L.nsteps;
@@ -355,7 +371,7 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  rc = choose_launch(pl, batch, hint, L);
+  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L);
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : pl->stream;
   return run(pl, L, batch, c0, beq, geom, switch_every, max_iters, tol, flags, c_out, hist, iters, conv, lam_out,
@@ -373,7 +389,7 @@ int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const 
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  rc = choose_launch(pl, batch, hint, L);
+  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L);
   if (rc) return rc;
   const int n = pl->n, nv = pl->nv, m = pl->m;
   const long long p = (long long)n * (n - 1) / 2 + (long long)n * pl->nobs;
