@@ -114,7 +114,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   const int NV = L.NVMAX;
   take(k.o_c, 3LL * n * NV);
   take(k.o_qp, (long long)NW * L.qslots * 3 * NP);
-  take(k.o_qsp, (long long)NW * L.qslots * 3 * 32);
+  take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
   take(k.o_P, (long long)L.tmax * NV);
   take(k.o_r1, (long long)C * L.own_max * 3 * NV);
   take(k.o_rS, (long long)C * 3 * NV);
@@ -156,7 +156,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
   } else {
     L.W = 32;
   }
-  L.nsteps = count_steps(n, pl->nobs, NB);
+  L.nsteps = std::max(1, count_steps(n, pl->nobs, NB));  // n = 1, no obstacles: one empty step
   const long long budget = pl->smem_optin / 8;
   std::vector<int> cands;
   if (hint > 0) {
