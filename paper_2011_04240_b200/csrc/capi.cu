@@ -115,6 +115,8 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_c, 3LL * n * NV);
   take(k.o_qp, (long long)NW * L.qslots * 3 * NP);
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
+  take(k.o_xw, (long long)NW * L.NB * 96);
+  take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.qslots) + 1) / 2);
   take(k.o_P, (long long)L.tmax * NV);
   take(k.o_r1, (long long)C * L.own_max * 3 * NV);
   take(k.o_rS, (long long)C * 3 * NV);
