@@ -53,7 +53,7 @@ const KernelEntry kKernels[] = {
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0, qslots = 0;
+  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0;
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -105,6 +105,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   L.tasks_max = ceil_div(L.tmax, TPW);               // time groups of the largest CTA
   const int spw = ceil_div(L.tasks_max * L.nsteps, NW);  // steps per warp (largest CTA)
   L.qslots = ceil_div(spw, L.nsteps) + 1;            // groups a warp can touch
+  L.wpg = std::min(NW, ceil_div(L.nsteps, spw) + 1);  // warps that can share a group
   L.own_max = ceil_div(n, C);
   long long o = 0;
   auto take = [&](int& off, long long cnt) {
@@ -116,7 +117,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_qp, (long long)NW * L.qslots * 3 * NP);
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
   take(k.o_xw, (long long)NW * L.NB * 96);
-  take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.qslots) + 1) / 2);
+  take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
   take(k.o_P, (long long)L.tmax * NV);
   take(k.o_r1, (long long)C * L.own_max * 3 * NV);
   take(k.o_rS, (long long)C * 3 * NV);
@@ -219,7 +220,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.n = pl->n; k.nobs = pl->nobs; k.m = pl->m; k.nv = pl->nv; k.S = pl->S;
   k.P = pl->P; k.G = pl->G; k.Gm = pl->Gm; k.F = pl->F; k.Fm = pl->Fm; k.E = pl->E; k.rho = pl->rho;
   k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
-  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots;
+  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots; k.wpg = L.wpg;
   k.B = batch; k.gstride = 2 + 5 * pl->nobs;
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
