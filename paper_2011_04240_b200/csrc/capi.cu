@@ -102,10 +102,17 @@ long long layout(st_plan* pl, Launch& L, int C) {
   const int NP = L.NB * 32, n = pl->n, NW = L.NT / 32, TPW = 32 / L.W;
   L.C = C;
   L.tmax = ceil_div(pl->m, C);
-  L.tasks_max = ceil_div(L.tmax, TPW);               // time groups of the largest CTA
-  const int spw = ceil_div(L.tasks_max * L.nsteps, NW);  // steps per warp (largest CTA)
-  L.qslots = ceil_div(spw, L.nsteps) + 1;            // groups a warp can touch
-  L.wpg = std::min(NW, ceil_div(L.nsteps, spw) + 1);  // warps that can share a group
+  L.tasks_max = ceil_div(L.tmax, TPW);  // time groups of the largest CTA
+  // A CTA owns floor(m/C) or ceil(m/C) samples; its warps split groups x steps evenly
+  // (work_split), so bound the slot counts over both cases.
+  L.qslots = 1;
+  L.wpg = 1;
+  for (int tc : {pl->m / C, L.tmax}) {
+    if (tc < 1) continue;
+    const int spw = ceil_div(ceil_div(tc, TPW) * L.nsteps, NW);
+    L.qslots = std::max(L.qslots, ceil_div(spw, L.nsteps) + 1);         // groups a warp can touch
+    L.wpg = std::max(L.wpg, std::min(NW, ceil_div(L.nsteps, spw) + 1));  // warps sharing one group
+  }
   L.own_max = ceil_div(n, C);
   long long o = 0;
   auto take = [&](int& off, long long cnt) {
