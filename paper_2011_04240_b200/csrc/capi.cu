@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -245,6 +246,12 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   } else {
     k.lam_ws = nullptr;
   }
+  // opt-in phase timers: SWARM_PHASE_TIMERS=1 prints per-phase cycles of scenario 0, CTA 0
+  static long long* d_ts = nullptr;
+  const bool timers = std::getenv("SWARM_PHASE_TIMERS") != nullptr;
+  if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 256 * 8 * sizeof(long long)));
+  if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 256 * 8 * sizeof(long long), s));
+  k.tstamp = timers ? d_ts : nullptr;
   ST_CUDA(cudaMemsetAsync(pl->d_counter, 0, sizeof(int), s));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(L.nclusters * L.C);
@@ -259,6 +266,28 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   cfg.attrs = at;
   cfg.numAttrs = 1;
   ST_CUDA(cudaLaunchKernelEx(&cfg, L.fn, k));
+  if (timers) {
+    std::vector<long long> h(256 * 8);
+    ST_CUDA(cudaMemcpyAsync(h.data(), d_ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int it = 1; it < 255 && h[8 * (it + 1)]; ++it, ++cnt) {
+      const long long* t = &h[8 * it];
+      acc[0] += t[1] - t[0];             // test + solve (owner)
+      acc[1] += t[2] - t[1];             // cluster barrier 2
+      acc[2] += t[3] - t[2];             // pairwise (warp 0)
+      acc[3] += t[4] - t[3];             // wait for slowest warp
+      acc[4] += t[5] - t[4];             // projection + push
+      acc[5] += h[8 * (it + 1)] - t[5];  // cluster barrier 1
+    }
+    if (cnt)
+      std::fprintf(stderr,
+                   "[swarm timers] C=%d NB=%d: cycles/iter solve %.0f | bar2 %.0f | pairwise(w0) %.0f | "
+                   "warp-wait %.0f | project %.0f | bar1 %.0f  (iters %d)\n",
+                   L.C, L.NB, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
+                   cnt);
+  }
   return 0;
 }
 
