@@ -126,14 +126,16 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
   take(k.o_xw, (long long)NW * L.NB * 96);
   take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
+  take(k.o_qc, (long long)L.tmax * 3 * n + 3LL * L.tmax);
   take(k.o_P, (long long)L.tmax * NV);
-  take(k.o_r1, (long long)C * L.own_max * 3 * NV);
-  take(k.o_rS, (long long)C * 3 * NV);
-  take(k.o_rN, 2LL * C);
-  take(k.o_rB, C);
+  take(k.o_Rp, 3LL * n * NV);
+  take(k.o_xch, 3LL * NV + 2);
+  k.xch_norm = 3 * NV;
+  take(k.o_cown, (long long)L.own_max * 3 * NV);
+  take(k.o_bw, NW);
   take(k.o_R, (long long)L.own_max * 3 * NV);
   take(k.o_Rb, 3LL * NV);
-  take(k.o_cl, (long long)L.own_max * 3 * NV);
+  take(k.o_mat, 2LL * NV * NV + 3LL * NV * 6);
   take(k.o_geo, 8 + 8LL * pl->nobs);
   take(k.o_beq, 18LL * L.own_max);
   take(k.o_bb, 18);
@@ -249,8 +251,8 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   // opt-in phase timers: SWARM_PHASE_TIMERS=1 prints per-phase cycles of scenario 0, CTA 0
   static long long* d_ts = nullptr;
   const bool timers = std::getenv("SWARM_PHASE_TIMERS") != nullptr;
-  if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 256 * 8 * sizeof(long long)));
-  if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 256 * 8 * sizeof(long long), s));
+  if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 256 * 16 * sizeof(long long)));
+  if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 256 * 16 * sizeof(long long), s));
   k.tstamp = timers ? d_ts : nullptr;
   ST_CUDA(cudaMemsetAsync(pl->d_counter, 0, sizeof(int), s));
   cudaLaunchConfig_t cfg = {};
@@ -267,26 +269,23 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   cfg.numAttrs = 1;
   ST_CUDA(cudaLaunchKernelEx(&cfg, L.fn, k));
   if (timers) {
-    std::vector<long long> h(256 * 8);
+    std::vector<long long> h(256 * 16);
     ST_CUDA(cudaMemcpyAsync(h.data(), d_ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
-    double acc[6] = {0, 0, 0, 0, 0, 0};
+    static const char* names[] = {"test", "solve:reduce", "solve:c+push", "solve:boundary", "bar2", "pairwise(w0)",
+                                  "warp-wait", "proj:rows", "proj:agent-sum", "proj:norms", "bar1"};
+    double acc[11] = {0};
     int cnt = 0;
-    for (int it = 1; it < 255 && h[8 * (it + 1)]; ++it, ++cnt) {
-      const long long* t = &h[8 * it];
-      acc[0] += t[1] - t[0];             // test + solve (owner)
-      acc[1] += t[2] - t[1];             // cluster barrier 2
-      acc[2] += t[3] - t[2];             // pairwise (warp 0)
-      acc[3] += t[4] - t[3];             // wait for slowest warp
-      acc[4] += t[5] - t[4];             // projection + push
-      acc[5] += h[8 * (it + 1)] - t[5];  // cluster barrier 1
+    for (int it = 1; it < 255 && h[16 * (it + 1)]; ++it, ++cnt) {
+      const long long* t = &h[16 * it];
+      for (int q = 0; q < 10; ++q) acc[q] += t[q + 1] - t[q];
+      acc[10] += h[16 * (it + 1)] - t[10];
     }
-    if (cnt)
-      std::fprintf(stderr,
-                   "[swarm timers] C=%d NB=%d: cycles/iter solve %.0f | bar2 %.0f | pairwise(w0) %.0f | "
-                   "warp-wait %.0f | project %.0f | bar1 %.0f  (iters %d)\n",
-                   L.C, L.NB, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
-                   cnt);
+    if (cnt) {
+      std::fprintf(stderr, "[swarm timers] C=%d NB=%d iters=%d cycles/iter:", L.C, L.NB, cnt);
+      for (int q = 0; q < 11; ++q) std::fprintf(stderr, " %s=%.0f", names[q], acc[q] / cnt);
+      std::fprintf(stderr, "\n");
+    }
   }
   return 0;
 }
