@@ -122,13 +122,18 @@ long long layout(st_plan* pl, Launch& L, int C) {
   };
   const int NV = L.NVMAX;
   take(k.o_c, 3LL * n * NV);
-  take(k.o_qp, (long long)NW * L.qslots * 3 * NP);
+  // Regions never live at the same time share storage:
+  //   qp (pairwise -> combine)  and  Rp (projection -> owners' pull, before the next pairwise)
+  //   xw (pairwise)             and  qc (combine -> projection)
+  const long long qp_sz = (long long)NW * L.qslots * 3 * NP, rp_sz = 3LL * n * NV;
+  take(k.o_qp, std::max(qp_sz, rp_sz));
+  k.o_Rp = k.o_qp;
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
-  take(k.o_xw, (long long)NW * L.NB * 96);
+  const long long xw_sz = (long long)NW * L.NB * 96, qc_sz = (long long)L.tmax * 3 * n + 3LL * L.tmax;
+  take(k.o_xw, std::max(xw_sz, qc_sz));
+  k.o_qc = k.o_xw;
   take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
-  take(k.o_qc, (long long)L.tmax * 3 * n + 3LL * L.tmax);
   take(k.o_P, (long long)L.tmax * NV);
-  take(k.o_Rp, 3LL * n * NV);
   take(k.o_xch, 3LL * NV + 2);
   k.xch_norm = 3 * NV;
   take(k.o_cown, (long long)L.own_max * 3 * NV);
