@@ -124,14 +124,14 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_c, 3LL * n * NV);
   // Regions never live at the same time share storage:
   //   qp (pairwise -> combine)  and  Rp (projection -> owners' pull, before the next pairwise)
-  //   xw (pairwise)             and  qc (combine -> projection)
   const long long qp_sz = (long long)NW * L.qslots * 3 * NP, rp_sz = 3LL * n * NV;
   take(k.o_qp, std::max(qp_sz, rp_sz));
   k.o_Rp = k.o_qp;
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
-  const long long xw_sz = (long long)NW * L.NB * 96, qc_sz = (long long)L.tmax * 3 * n + 3LL * L.tmax;
-  take(k.o_xw, std::max(xw_sz, qc_sz));
-  k.o_qc = k.o_xw;
+  //   X (positions -> pairwise)  and  qc (combine -> projection)
+  const long long x_sz = (long long)L.tasks_max * 3 * NP, qc_sz = (long long)L.tmax * 3 * n + 3LL * L.tmax;
+  take(k.o_X, std::max(x_sz, qc_sz));
+  k.o_qc = k.o_X;
   take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
   take(k.o_P, (long long)L.tmax * NV);
   take(k.o_xch, 3LL * NV + 2);
