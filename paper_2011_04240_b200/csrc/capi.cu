@@ -65,8 +65,8 @@ struct Launch {
 
 struct st_plan {
   int n, nobs, m, nv, S, device, nvmax;
-  double* d_mats = nullptr;  // P | G | Gm | F | Fm | E | rho
-  const double *P, *G, *Gm, *F, *Fm, *E, *rho;
+  double* d_mats = nullptr;  // P | G | Gm | F | Fm | E | rho | packed stage mats | 1/rho
+  const double *P, *G, *Gm, *F, *Fm, *E, *rho, *mats, *inv_rho;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int* d_counter = nullptr;
@@ -134,13 +134,14 @@ long long layout(st_plan* pl, Launch& L, int C) {
   k.o_qc = k.o_X;
   take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
   take(k.o_P, (long long)L.tmax * NV);
-  take(k.o_xch, 3LL * NV + 2);
+  take(k.o_xch, 3LL * NV + 4);  // agent sums | sum r^2, max |r| | boundary max x 2 parities
   k.xch_norm = 3 * NV;
   take(k.o_cown, (long long)L.own_max * 3 * NV);
-  take(k.o_bw, NW);
+  take(k.o_nrm, 3LL * C);
+  take(k.o_otab, (n + 1) / 2);
   take(k.o_R, (long long)L.own_max * 3 * NV);
   take(k.o_Rb, 3LL * NV);
-  take(k.o_mat, 2LL * NV * NV + 3LL * NV * 6);
+  take(k.o_mat, NV == 12 ? swarm::StageMats<12>::SIZE : swarm::StageMats<16>::SIZE);
   take(k.o_geo, 8 + 8LL * pl->nobs);
   take(k.o_beq, 18LL * L.own_max);
   take(k.o_bb, 18);
@@ -234,6 +235,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   swarm::KParams& k = L.kp;
   k.n = pl->n; k.nobs = pl->nobs; k.m = pl->m; k.nv = pl->nv; k.S = pl->S;
   k.P = pl->P; k.G = pl->G; k.Gm = pl->Gm; k.F = pl->F; k.Fm = pl->Fm; k.E = pl->E; k.rho = pl->rho;
+  k.mats = pl->mats; k.inv_rho = pl->inv_rho;
   k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
   k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots; k.wpg = L.wpg;
   k.B = batch; k.gstride = 2 + 5 * pl->nobs;
@@ -277,18 +279,18 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
     std::vector<long long> h(256 * 16);
     ST_CUDA(cudaMemcpyAsync(h.data(), d_ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
-    static const char* names[] = {"test", "solve:reduce", "solve:c+push", "solve:boundary", "bar2", "pairwise(w0)",
-                                  "warp-wait", "proj:rows", "proj:agent-sum", "proj:norms", "bar1"};
-    double acc[11] = {0};
+    static const char* names[] = {"pull+test", "solve", "bar2", "gather", "positions", "pairwise", "warp-wait",
+                                  "project", "bar1"};
+    double acc[9] = {0};
     int cnt = 0;
     for (int it = 1; it < 255 && h[16 * (it + 1)]; ++it, ++cnt) {
       const long long* t = &h[16 * it];
-      for (int q = 0; q < 10; ++q) acc[q] += t[q + 1] - t[q];
-      acc[10] += h[16 * (it + 1)] - t[10];
+      for (int q = 0; q < 8; ++q) acc[q] += t[q + 1] - t[q];
+      acc[8] += h[16 * (it + 1)] - t[8];
     }
     if (cnt) {
       std::fprintf(stderr, "[swarm timers] C=%d NB=%d iters=%d cycles/iter:", L.C, L.NB, cnt);
-      for (int q = 0; q < 11; ++q) std::fprintf(stderr, " %s=%.0f", names[q], acc[q] / cnt);
+      for (int q = 0; q < 9; ++q) std::fprintf(stderr, " %s=%.0f", names[q], acc[q] / cnt);
       std::fprintf(stderr, "\n");
     }
   }
@@ -348,6 +350,40 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
   put(Fm, S, nv, 6, NV, 6);
   put(E, 1, 6, nv, 6, NV);
   put(rho, 1, 1, S, 1, S);
+  // per-stage packed shared-memory image: G Gm F Fm EG EGm EF EFm rho 1/rho (StageMats layout)
+  const int MS = NV == 12 ? swarm::StageMats<12>::SIZE : swarm::StageMats<16>::SIZE;
+  const int oG = 0, oGm = NV * NV, oF = 2 * NV * NV, oFm = oF + NV * 6, oEG = oFm + NV * 6, oEGm = oEG + 6 * NV,
+            oEF = oEGm + 6 * NV, oEFm = oEF + 36, oR = oEFm + 36;
+  h.resize(total + (size_t)S * MS + S, 0.0);
+  for (int st = 0; st < S; ++st) {
+    double* d = h.data() + total + (size_t)st * MS;
+    const double* g = G + (size_t)st * nv * nv;
+    const double* gm = Gm + (size_t)st * nv * nv;
+    const double* f = F + (size_t)st * nv * 6;
+    const double* fm = Fm + (size_t)st * nv * 6;
+    for (int a = 0; a < nv; ++a) {
+      for (int b = 0; b < nv; ++b) { d[oG + a * NV + b] = g[a * nv + b]; d[oGm + a * NV + b] = gm[a * nv + b]; }
+      for (int e = 0; e < 6; ++e) { d[oF + a * 6 + e] = f[a * 6 + e]; d[oFm + a * 6 + e] = fm[a * 6 + e]; }
+    }
+    for (int e = 0; e < 6; ++e) {
+      for (int b = 0; b < nv; ++b) {
+        double sg = 0.0, sgm = 0.0;
+        for (int a = 0; a < nv; ++a) { sg += E[e * nv + a] * g[a * nv + b]; sgm += E[e * nv + a] * gm[a * nv + b]; }
+        d[oEG + e * NV + b] = sg;
+        d[oEGm + e * NV + b] = sgm;
+      }
+      for (int f2 = 0; f2 < 6; ++f2) {
+        double sf = 0.0, sfm = 0.0;
+        for (int a = 0; a < nv; ++a) { sf += E[e * nv + a] * f[a * 6 + f2]; sfm += E[e * nv + a] * fm[a * 6 + f2]; }
+        d[oEF + e * 6 + f2] = sf;
+        d[oEFm + e * 6 + f2] = sfm;
+      }
+    }
+    d[oR] = rho[st];
+    d[oR + 1] = 1.0 / rho[st];
+    h[total + (size_t)S * MS + st] = 1.0 / rho[st];
+  }
+  const size_t total_all = h.size();
   auto cleanup = [&](int code) {
     if (pl->d_mats) cudaFree(pl->d_mats);
     if (pl->d_counter) cudaFree(pl->d_counter);
@@ -355,8 +391,8 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
     delete pl;
     return code;
   };
-  cudaError_t e = cudaMalloc(&pl->d_mats, total * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemcpy(pl->d_mats, h.data(), total * sizeof(double), cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMalloc(&pl->d_mats, total_all * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(pl->d_mats, h.data(), total_all * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_counter, sizeof(int));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&pl->ev[i]);
@@ -372,7 +408,9 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
   pl->F = b; b += nF;
   pl->Fm = b; b += nF;
   pl->E = b; b += nE;
-  pl->rho = b;
+  pl->rho = b; b += S;
+  pl->mats = b; b += (size_t)S * MS;
+  pl->inv_rho = b;
   *out = pl;
   return ST_OK;
 }
