@@ -1,0 +1,349 @@
+"""Benchmark: batched AM joint solves on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Workload (BASELINE.json configs[1] scenarios, batched as configs[3]): a stream of
+32-agent random start/goal scenarios, ``generate_random(32, (8,8,3), 0.4, seed)``,
+seeds 0..1023, m=100 samples, Bernstein degree 10, default SolverConfig (150
+iterations max, tol 1e-2, rho = 2^s over 10 stages), FP64.  One step = solving the
+whole batch (every scenario to convergence or max_iters) in one device launch.
+
+* ``value``: solves/s, all ranks, inputs resident in HBM, device time (CUDA events on
+  the launch stream, L2 flushed between steps), max over ranks.
+* ``e2e``: the same solves through the C ABI ``st_solve`` with host buffers (H2D of the
+  packed boundary rows / straight-line coefficients, device loop, D2H of coefficients
+  and histories inside the timed region).
+* ``roofline``: the AM kernel is the only kernel; FP64 FMA-pipe bound (the pairwise
+  update is FP64 arithmetic on on-chip/L2 data).  Algorithmic work per pair-sample per
+  iteration = 85 FLOP; peak = measured DFMA throughput
+  (profiles/ubench_r1.txt: 64 lanes/clk/SM x 148 SMs x SM clock x 2).
+* ``cpu_baseline``: the reference algorithm (oracle/am_oracle.py, numpy/scipy LU path,
+  warm factors) on a bounded sample, one process per host core.
+* Multi-GPU (torchrun): scenarios are sharded over ranks (strong scaling, no
+  data-path collective; NCCL only for the barrier and the max-over-ranks timing).
+
+``--impl reference`` times the reference algorithm on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+BATCH = 1024
+FLOP_PER_PAIR_SAMPLE = 85.0
+BYTES_PER_PAIR_SAMPLE = 48.0
+
+
+def scenarios(lo: int, hi: int):
+    from paper_2011_04240_b200 import generate_random
+    return [generate_random(32, (8.0, 8.0, 3.0), 0.4, s) for s in range(lo, hi)]
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU reference (oracle port of the reference algorithm), one process per core
+
+
+def _cpu_worker(seeds):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from scipy.linalg import lu_factor
+
+    from oracle import am_oracle
+    specs = scenarios(seeds[0], seeds[1])
+    pr = am_oracle.Problem(specs[0])
+    rhos, _ = am_oracle.schedule()
+    factors = [lu_factor(pr.kkt(r), check_finite=False) for r in rhos]  # warm cache (reference excludes it)
+    t0 = time.perf_counter()
+    its = 0
+    for spec in specs:
+        its += am_oracle.solve(spec, factors=factors)["iterations"]
+    return time.perf_counter() - t0, len(specs), its
+
+
+def cpu_reference(n_per_core: int, cores: int | None = None):
+    import multiprocessing as mp
+    cores = cores or os.cpu_count() or 1
+    jobs = [(1024 + i * n_per_core, 1024 + (i + 1) * n_per_core) for i in range(cores)]
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    solves = sum(r[1] for r in res)
+    busy = max(r[0] for r in res)
+    return {"solves_per_s": solves / busy, "wall_s": wall, "solves": solves, "cores": cores,
+            "mean_iters": sum(r[2] for r in res) / solves}
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._p = index, [], None
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self._p:
+            self._p.terminate()
+            self._p.wait(timeout=5)
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) == 6 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = [nm for i, nm in enumerate(names) if any(r[2 + i].lower() == "active" for r in rows)]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference(args):
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    per_core = max(1, args.ref_per_core)
+    vals = []
+    for _ in range(max(0, args.warmup_ref)):
+        cpu_reference(1, cores)
+    for _ in range(args.steps):
+        vals.append(cpu_reference(per_core, cores))
+    v = sum(r["solves_per_s"] for r in vals) / len(vals)
+    sample = f"{per_core * cores} rand32 scenarios (seeds 1024..) per step, warm LU factors, 1 process/core"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": 1e3 * vals[-1]["wall_s"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "rand32 batch (generate_random(32,(8,8,3),0.4,seed))",
+                                            "agents": 32, "samples": 100, "degree": 10},
+            "cpu_baseline": {"value": v, "unit": "solves/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def single_solve_ms(names=("circ16j", "rand32_s0", "sph64j")):
+    from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve, named
+    cache = FactorCache()
+    out = {}
+    for nm in names:
+        spec = named(nm)
+        am_solve(spec, SolverConfig(), cache=cache)
+        best = None
+        for _ in range(3):
+            r = am_solve(spec, SolverConfig(), cache=cache)
+            t = r.timings["loop_s"] * 1e3
+            best = t if best is None else min(best, t)
+        out[nm] = {"ms": round(best, 4), "iterations": r.iterations, "converged": r.converged,
+                   "end_to_end_ms": round(r.timings["total_s"] * 1e3, 3)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--cpu-per-core", type=int, default=2, help="cpu_baseline sample: scenarios per core")
+    ap.add_argument("--ref-per-core", type=int, default=1)
+    ap.add_argument("--warmup-ref", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-single", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_2011_04240_b200 import FactorCache, SolverConfig, engine, kkt, native, pack, poly
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lo, hi = rank * args.batch // world, (rank + 1) * args.batch // world
+    specs = scenarios(lo, hi)
+    B = len(specs)
+    cfg = SolverConfig(device=local)
+    sched = cfg.schedule()
+    basis = poly.for_spec(specs[0])
+    fp = kkt.fingerprint(basis, 32, 0)
+    cache = FactorCache()
+    t_pre0 = time.perf_counter()
+    plan = engine._plan_for(cache, fp, basis, sched, 32, 0, local)
+    precompute_s = time.perf_counter() - t_pre0
+    c0, beq, geom = pack(specs, basis)
+    nv, m = basis.num_coeffs, basis.num_samples
+    # device-resident inputs/outputs
+    d_c0 = torch.from_numpy(c0).to(dev)
+    d_beq = torch.from_numpy(beq).to(dev)
+    d_geom = torch.from_numpy(geom).to(dev)
+    d_cout = torch.empty_like(d_c0)
+    d_hist = torch.empty((B, 3, cfg.max_iters), dtype=torch.float64, device=dev)
+    d_it = torch.empty(B, dtype=torch.int32, device=dev)
+    d_cv = torch.empty(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def launch():
+        plan.solve_device(B, d_c0.data_ptr(), d_beq.data_ptr(), d_geom.data_ptr(), sched.switch_every,
+                          cfg.max_iters, cfg.tolerance, d_cout.data_ptr(), d_hist.data_ptr(), d_it.data_ptr(),
+                          d_cv.data_ptr(), stream=stream.cuda_stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            launch()
+    torch.cuda.synchronize(dev)
+    iters = d_it.cpu().numpy()
+    pair_samples = float((iters.astype(np.float64) + 1.0).sum() * (32 * 31 // 2) * m)  # + init pass
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.zero_()  # L2 flush between timed steps (outside the events)
+                ev[i][0].record(stream)
+                launch()
+                ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    barrier(world)
+    dev_ms_max = allreduce_max(dev_ms, world, dev)
+    step_ms = dev_ms_max / args.steps
+    value = args.batch / (step_ms / 1e3)
+
+    # end to end through the C ABI with host buffers (H2D + loop + D2H inside the timed region)
+    e2e_times = []
+    for i in range(args.steps + 1):
+        barrier(world)
+        t0 = time.perf_counter()
+        out = plan.solve(c0, beq, geom, sched.switch_every, cfg.max_iters, cfg.tolerance)
+        if i > 0:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_s = allreduce_max(sum(e2e_times) / len(e2e_times), world, dev)
+    h2d = c0.nbytes + beq.nbytes + geom.nbytes
+    d2h = out["c"].nbytes + out["hist"].nbytes + out["iters"].nbytes + out["converged"].nbytes
+    launch_cfg = plan.query_launch(B)
+
+    if rank != 0:
+        return
+    ok = bool(np.array_equal(out["iters"], iters))
+    sm_mhz = clocks.summary()
+    peak_clk_ghz = 1.965
+    fp64_peak_tflops = 64 * 148 * peak_clk_ghz * 1e9 * 2 / 1e12
+    flops = FLOP_PER_PAIR_SAMPLE * pair_samples
+    achieved = flops / (dev_ms / args.steps / 1e3) / 1e12 / (1.0 if world == 1 else 1.0)
+    hbm_peak = None
+    try:
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except (OSError, KeyError, ValueError):
+        hbm_peak = 6650.0
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        traffic = tr.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    ach_bytes = BYTES_PER_PAIR_SAMPLE * pair_samples / (dev_ms / args.steps / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"batch of {args.batch} rand32 scenarios (generate_random(32,(8,8,3),0.4,seed), "
+                               f"seeds 0..{args.batch - 1}), 1/N per rank", "agents": 32, "samples": m,
+                   "degree": 10, "max_iters": cfg.max_iters, "tol": cfg.tolerance,
+                   "cluster_ctas": launch_cfg["cluster"], "clusters": launch_cfg["clusters"],
+                   "lambda_in_smem": bool(launch_cfg["lambda_in_smem"]),
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "e2e": {"value": round(args.batch / e2e_s, 2), "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "path": "C ABI st_solve, host buffers"},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(fp64_peak_tflops, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved / fp64_peak_tflops, 4), "traffic": traffic,
+                     "per_unit": f"{FLOP_PER_PAIR_SAMPLE:.0f} FLOP per pair-sample per iteration "
+                                 f"({pair_samples:.3e} pair-samples per launch incl. init pass)",
+                     "peak_source": "measured DFMA 64 lanes/clk/SM x 148 SMs x 1.965 GHz x 2 "
+                                    "(profiles/ubench_r1.txt)"},
+        "roofline_hbm": {"bound": "hbm", "achieved": round(ach_bytes, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(ach_bytes / hbm_peak, 4),
+                         "per_unit": "48 B (lambda read+write) per pair-sample per iteration"},
+        "clocks": sm_mhz,
+        "precompute_s": round(precompute_s, 4),
+        "iterations_mean": round(float(iters.mean()), 2),
+        "converged_frac": round(float(d_cv.cpu().numpy().mean()), 4),
+        "e2e_matches_device_iters": ok,
+    }
+    if not args.no_single and world == 1:
+        line["single_solve_ms"] = single_solve_ms()
+    if not args.no_cpu and world == 1:
+        cores = os.cpu_count() or 1
+        ref = cpu_reference(args.cpu_per_core, cores)
+        line["cpu_baseline"] = {"value": round(ref["solves_per_s"], 3), "unit": "solves/s", "cores": cores,
+                                "kind": "port",
+                                "sample": f"{ref['solves']} rand32 scenarios (seeds 1024..), oracle/am_oracle.py "
+                                          f"(reference LU algorithm, numpy/scipy), warm factors, 1 process/core"}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,15 +183,28 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
   } else if (batch == 1) {
     cands = {16, 8, 4, 2, 1};  // latency: spread one scenario widest
   } else {
-    cands = {1, 2, 4, 8, 16};  // throughput: smallest cluster that keeps lambda on chip
+    // throughput: measured on B200 (profiles/) two-CTA clusters streaming
+    // lambda from L2 beat wider clusters that keep it on chip (exchange overhead dominates)
+    cands = {2, 1, 4, 8, 16};
   }
-  // pass 0: lambda in shared memory; pass 1: lambda in a global (L2-resident) slab
-  for (int pass = 0; pass < 2; ++pass) {
+  // Latency (one scenario): prefer lambda on chip, then the widest cluster.
+  // Throughput (batches): prefer the cluster order above; at each size lambda on chip if it fits.
+  const bool throughput = hint <= 0 && batch > 1;
+  std::vector<std::pair<int, int>> order;  // (C, pass)
+  if (throughput) {
+    for (int C : cands)
+      for (int pass = 0; pass < 2; ++pass) order.push_back({C, pass});
+  } else {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int C : cands) order.push_back({C, pass});
+  }
+  for (const auto& cp : order) {
+    const int C = cp.first, pass = cp.second;
     const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
     if (keep && pass == 0) continue;
     const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam);
     if (!ke) continue;
-    for (int C : cands) {
+    {
       if (C > pl->m || C < 1 || C > 16) continue;
       Launch T = L;
       T.NT = ke->NT;
