@@ -54,7 +54,7 @@ const KernelEntry kKernels[] = {
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0;
+  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0;
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -72,6 +72,8 @@ struct st_plan {
   int* d_counter = nullptr;
   double* d_lam = nullptr;
   size_t lam_bytes = 0;
+  double* d_cws = nullptr;
+  size_t c_bytes = 0;
   void* d_io = nullptr;  // inputs+outputs of host-pointer solves
   size_t io_bytes = 0;
   int smem_optin = 0;
@@ -121,7 +123,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
     o += (cnt + 1) & ~1LL;  // keep 16-byte alignment
   };
   const int NV = L.NVMAX;
-  take(k.o_c, 3LL * n * NV);
+  take(k.o_c, L.c_global ? 0 : 3LL * n * NV);
   // Regions never live at the same time share storage:
   //   qp (pairwise -> combine)  and  Rp (projection -> owners' pull, before the next pairwise)
   const long long qp_sz = (long long)NW * L.qslots * 3 * NP, rp_sz = 3LL * n * NV;
@@ -198,8 +200,10 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
     for (int pass = 0; pass < 2; ++pass)
       for (int C : cands) order.push_back({C, pass});
   }
+  for (int cg_try = 0; cg_try < 2; ++cg_try)
   for (const auto& cp : order) {
     const int C = cp.first, pass = cp.second;
+    if (cg_try == 1 && pass == 0) continue;  // coefficients in global memory only with lambda there too
     const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
     if (keep && pass == 0) continue;
     const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam);
@@ -209,6 +213,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
       Launch T = L;
       T.NT = ke->NT;
       T.fn = ke->fn;
+      T.c_global = cg_try;
       const long long base = layout(pl, T, C);
       const long long need = base + (pass == 0 ? T.lam_per_cta : 0);
       if (need > budget) continue;
@@ -255,6 +260,19 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
   k.switch_every = switch_every; k.max_iters = max_iters; k.flags = flags; k.tol = tol;
+  k.c_global = L.c_global;
+  k.c_ws = nullptr;
+  if (L.c_global) {
+    const size_t need = (size_t)L.nclusters * 3 * pl->n * L.NVMAX * sizeof(double);
+    if (need > pl->c_bytes) {
+      if (pl->d_cws) cudaFree(pl->d_cws);
+      pl->d_cws = nullptr;
+      pl->c_bytes = 0;
+      ST_CUDA(cudaMalloc(&pl->d_cws, need));
+      pl->c_bytes = need;
+    }
+    k.c_ws = pl->d_cws;
+  }
   if (!L.lam_smem) {
     const size_t need = (size_t)L.nclusters * L.C * L.lam_per_cta * sizeof(double);
     if (need > pl->lam_bytes) {
@@ -437,6 +455,7 @@ int st_plan_destroy(st_plan* pl) {
   if (pl->d_mats) cudaFree(pl->d_mats);
   if (pl->d_counter) cudaFree(pl->d_counter);
   if (pl->d_lam) cudaFree(pl->d_lam);
+  if (pl->d_cws) cudaFree(pl->d_cws);
   if (pl->d_io) cudaFree(pl->d_io);
   if (pl->stream) cudaStreamDestroy(pl->stream);
   delete pl;
