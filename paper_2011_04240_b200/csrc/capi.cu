@@ -54,7 +54,7 @@ const KernelEntry kKernels[] = {
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0;
+  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1;
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -74,6 +74,8 @@ struct st_plan {
   size_t lam_bytes = 0;
   double* d_cws = nullptr;
   size_t c_bytes = 0;
+  void* d_rg = nullptr;
+  size_t rg_bytes = 0;
   void* d_io = nullptr;  // inputs+outputs of host-pointer solves
   size_t io_bytes = 0;
   int smem_optin = 0;
@@ -104,13 +106,14 @@ long long layout(st_plan* pl, Launch& L, int C) {
   swarm::KParams& k = L.kp;
   const int NP = L.NB * 32, n = pl->n, NW = L.NT / 32, TPW = 32 / L.W;
   L.C = C;
-  L.tmax = ceil_div(pl->m, C);
+  const int KC = L.K * C;  // CTAs sharing one scenario
+  L.tmax = ceil_div(pl->m, KC);
   L.tasks_max = ceil_div(L.tmax, TPW);  // time groups of the largest CTA
   // A CTA owns floor(m/C) or ceil(m/C) samples; its warps split groups x steps evenly
   // (work_split), so bound the slot counts over both cases.
   L.qslots = 1;
   L.wpg = 1;
-  for (int tc : {pl->m / C, L.tmax}) {
+  for (int tc : {pl->m / KC, L.tmax}) {
     if (tc < 1) continue;
     const int spw = ceil_div(ceil_div(tc, TPW) * L.nsteps, NW);
     L.qslots = std::max(L.qslots, ceil_div(spw, L.nsteps) + 1);         // groups a warp can touch
@@ -239,6 +242,21 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
         continue;
       }
       T.nclusters = std::min(batch, active);
+      // one large scenario: spread it over every co-resident cluster (grid barrier per iteration)
+      const char* mc = std::getenv("SWARM_MULTI_CLUSTER");
+      const bool multi = batch == 1 && C > 1 && active > 1 && (mc ? std::atoi(mc) != 0 : pl->n > 32);
+      if (multi) {
+        Launch M = T;
+        M.K = std::min(active, std::max(1, pl->m / C));
+        const long long mbase = layout(pl, M, C);
+        const long long mneed = mbase + (pass == 0 ? M.lam_per_cta : 0);
+        if (mneed <= budget) {
+          M.smem_bytes = (size_t)mneed * 8;
+          ST_CUDA(cudaFuncSetAttribute(M.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M.smem_bytes));
+          M.nclusters = M.K;
+          T = M;
+        }
+      }
       L = T;
       return 0;
     }
@@ -260,6 +278,22 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
   k.switch_every = switch_every; k.max_iters = max_iters; k.flags = flags; k.tol = tol;
+  k.K = L.K;
+  k.Rg = nullptr;
+  k.gbar = nullptr;
+  if (L.K > 1) {
+    const size_t need = (size_t)L.K * (3 * (size_t)pl->n * L.NVMAX + 3 * L.NVMAX + 4) * sizeof(double) + 64;
+    if (need > pl->rg_bytes) {
+      if (pl->d_rg) cudaFree(pl->d_rg);
+      pl->d_rg = nullptr;
+      pl->rg_bytes = 0;
+      ST_CUDA(cudaMalloc(&pl->d_rg, need));
+      pl->rg_bytes = need;
+    }
+    k.gbar = reinterpret_cast<unsigned*>(pl->d_rg);
+    k.Rg = reinterpret_cast<double*>(reinterpret_cast<char*>(pl->d_rg) + 64);
+    ST_CUDA(cudaMemsetAsync(pl->d_rg, 0, 64, s));
+  }
   k.c_global = L.c_global;
   k.c_ws = nullptr;
   if (L.c_global) {
@@ -456,6 +490,7 @@ int st_plan_destroy(st_plan* pl) {
   if (pl->d_counter) cudaFree(pl->d_counter);
   if (pl->d_lam) cudaFree(pl->d_lam);
   if (pl->d_cws) cudaFree(pl->d_cws);
+  if (pl->d_rg) cudaFree(pl->d_rg);
   if (pl->d_io) cudaFree(pl->d_io);
   if (pl->stream) cudaStreamDestroy(pl->stream);
   delete pl;

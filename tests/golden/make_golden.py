@@ -24,7 +24,7 @@ import shutil
 import sys
 import time
 
-os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "8" if "--big" in sys.argv else "1")
 import numpy as np  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -128,6 +128,9 @@ def scenarios(st):
                                                         basis_kind=st.BasisKind.MONOMIAL, degree=6),
                                     {"max_iters": 6}, False),
         "obs8_state": (P.generate_random_with_obstacles(8, (8, 8, 3), 0.4, 4, 0.5, 1), {}, True),
+        # large fleets (slow on the reference: minutes); BASELINE config 5 and an NB=4 case
+        "rand128_s0": (P.generate_random(128, (20, 20, 6), 0.4, 0), {}, False),
+        "rand256_s0": (P.generate_random(256, (20, 20, 6), 0.4, 0), {}, False),
     }
     return out
 
@@ -149,6 +152,7 @@ def run(st, spec, kwargs, keep, perturb=False):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*")
+    ap.add_argument("--big", action="store_true", help="large fleets with 8 BLAS threads")
     args = ap.parse_args()
     st = import_reference()
     for name, (spec, kwargs, keep) in scenarios(st).items():
