@@ -177,7 +177,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def single_solve_ms(names=("circ16j", "rand32_s0", "sph64j")):
+def single_solve_ms(names=("circ16j", "rand32_s0", "sph64j", "rand256_s0")):
     from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve, named
     cache = FactorCache()
     out = {}

@@ -158,6 +158,8 @@ def main():
     for name, (spec, kwargs, keep) in scenarios(st).items():
         if args.only and name not in args.only:
             continue
+        if not args.only and not args.big and len(spec.start) > 64:
+            continue  # large fleets take minutes on the reference: regenerate with --big
         t0 = time.time()
         rep = run(st, spec, kwargs, keep)
         noisy = run(st, spec, kwargs, False, perturb=True)

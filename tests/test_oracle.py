@@ -11,7 +11,7 @@ import pytest
 from conftest import CHAOTIC, coeff_tol, golden_names, load_golden, rel_err
 from oracle import am_oracle
 
-FAST = [n for n in golden_names() if n not in ("sph64j", "rand48_s0")]
+FAST = [n for n in golden_names() if n not in ("sph64j", "rand48_s0", "rand128_s0", "rand256_s0")]
 
 
 def _kw(cfg):
