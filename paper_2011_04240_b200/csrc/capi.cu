@@ -54,7 +54,7 @@ const KernelEntry kKernels[] = {
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1;
+  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_smem_groups = 0;
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -221,7 +221,18 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
       const long long need = base + (pass == 0 ? T.lam_per_cta : 0);
       if (need > budget) continue;
       T.lam_smem = pass == 0 ? 1 : 0;
-      T.smem_bytes = (size_t)need * 8;
+      T.lam_smem_groups = 0;
+      long long need2 = need;
+      if (pass == 1 && !keep) {
+        // hybrid: spare shared memory holds the first groups of lambda (the rest stays in L2)
+        const long long per_group = (long long)T.nsteps * 96;
+        const char* hy = std::getenv("SWARM_LAM_HYBRID");
+        if (!hy || std::atoi(hy) != 0) {
+          T.lam_smem_groups = (int)std::min<long long>(T.tasks_max, (budget - need) / per_group);
+          need2 = need + (long long)T.lam_smem_groups * per_group;
+        }
+      }
+      T.smem_bytes = (size_t)need2 * 8;
       ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_bytes));
       cudaLaunchConfig_t cfg = {};
@@ -249,7 +260,13 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
         Launch M = T;
         M.K = std::min(active, std::max(1, pl->m / C));
         const long long mbase = layout(pl, M, C);
-        const long long mneed = mbase + (pass == 0 ? M.lam_per_cta : 0);
+        long long mneed = mbase + (pass == 0 ? M.lam_per_cta : 0);
+        M.lam_smem_groups = 0;
+        if (pass == 1 && !keep && mneed <= budget) {
+          const long long per_group = (long long)M.nsteps * 96;
+          M.lam_smem_groups = (int)std::min<long long>(M.tasks_max, (budget - mneed) / per_group);
+          mneed += (long long)M.lam_smem_groups * per_group;
+        }
         if (mneed <= budget) {
           M.smem_bytes = (size_t)mneed * 8;
           ST_CUDA(cudaFuncSetAttribute(M.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M.smem_bytes));
@@ -274,6 +291,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.mats = pl->mats; k.inv_rho = pl->inv_rho;
   k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
   k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots; k.wpg = L.wpg;
+  k.lam_smem_groups = L.lam_smem_groups;
   k.B = batch; k.gstride = 2 + 5 * pl->nobs;
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
@@ -317,6 +335,31 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       pl->lam_bytes = need;
     }
     k.lam_ws = pl->d_lam;
+    // keep the lambda slabs resident in L2 (persisting window) unless disabled
+    const char* pe = std::getenv("SWARM_L2_PERSIST");
+    if (!pe || std::atoi(pe) != 0) {
+      int dev = 0, max_persist = 0, max_window = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      const size_t used = (size_t)L.nclusters * L.C * L.lam_per_cta * sizeof(double);
+      const double gfrac = L.tasks_max > 0 ? 1.0 - (double)L.lam_smem_groups / L.tasks_max : 1.0;
+      if (max_persist > 0 && max_window > 0) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+        cudaStreamAttrValue av = {};
+        av.accessPolicyWindow.base_ptr = pl->d_lam;
+        av.accessPolicyWindow.num_bytes = std::min(used, (size_t)max_window);
+        av.accessPolicyWindow.hitRatio =
+            (float)std::min(1.0, (double)max_persist / std::max(1.0, gfrac * av.accessPolicyWindow.num_bytes));
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
+        cudaGetLastError();
+        if (std::getenv("SWARM_VERBOSE"))
+          std::fprintf(stderr, "[swarm] L2 persisting: max %d B, window max %d B, lambda %zu B, smem groups %d/%d\n",
+                       max_persist, max_window, used, L.lam_smem_groups, L.tasks_max);
+      }
+    }
   } else {
     k.lam_ws = nullptr;
   }
