@@ -300,7 +300,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.Rg = nullptr;
   k.gbar = nullptr;
   if (L.K > 1) {
-    const size_t need = (size_t)L.K * (3 * (size_t)pl->n * L.NVMAX + 3 * L.NVMAX + 4) * sizeof(double) + 64;
+    const size_t need = 2 * (size_t)L.K * (3 * (size_t)pl->n * L.NVMAX + 3 * L.NVMAX + 4) * sizeof(double) + 64;
     if (need > pl->rg_bytes) {
       if (pl->d_rg) cudaFree(pl->d_rg);
       pl->d_rg = nullptr;
