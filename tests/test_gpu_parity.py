@@ -143,3 +143,19 @@ def test_chaotic_instances_still_meet_acceptance(cuda_ok):
         rep = am_solve(spec)
         assert rep.converged
         assert rep.metrics["min_normalized_distance"] >= 0.95
+
+
+@pytest.mark.parametrize("name", ["rand48_s0", "rand20_s0", "obs8", "circ16j"])
+def test_results_independent_of_stale_device_memory(cuda_ok, name):
+    """Poison freed device memory with NaN bit patterns first: no kernel may read a slot it did not write."""
+    import torch
+
+    from paper_2011_04240_b200 import FactorCache, am_solve
+    junk = torch.full((256 * 1024 * 1024,), float("nan"), dtype=torch.float64, device="cuda")  # 2 GiB
+    del junk
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # hand the poisoned pages back to the driver
+    spec, cfg, ref = load_golden(name)
+    rep = am_solve(spec, _config(cfg), cache=FactorCache())
+    assert rep.iterations == int(ref["iterations"])
+    assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref)
