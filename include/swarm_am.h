@@ -78,6 +78,27 @@ int st_solve_device(st_plan* plan, int batch, const double* c0, const double* b_
                     int cluster_hint, double* c_out, double* hist, int* iters, int* converged,
                     double* lam_out, double* d_out, void* stream);
 
+/* ---- Pair-sharded solve of ONE large scenario over G GPUs (BASELINE config 5).
+ * Replaces nothing in the reference (single process, CPU); it is the north star's
+ * "very large n shards the agent pairs across GPUs": every GPU owns a contiguous
+ * slice of the time samples (all agent pairs at those samples), the per-iteration
+ * exchange of the 3 x n x n_v partial right-hand sides (plus residual norms) goes
+ * through peer-mapped buffers inside the one persistent kernel, summed in a fixed
+ * participant order (identical on every GPU).  One process per GPU:
+ *   st_shard_layout  -> cluster size, clusters per GPU, buffer bytes, participants
+ *   st_shard_buffer  -> allocate this GPU's buffer and export its IPC handle
+ *   st_shard_open    -> map a peer's buffer (cudaIpcOpenMemHandle)
+ *   st_shard_reset   -> rank 0 zeroes the barrier word (host barrier before launching)
+ *   st_solve_sharded -> every rank launches; outputs are written on rank 0 */
+int st_shard_layout(st_plan* plan, int G, long long* out4);
+int st_shard_buffer(st_plan* plan, long long bytes, void** dptr, unsigned char* handle64);
+int st_shard_open(st_plan* plan, const unsigned char* handle64, void** dptr);
+int st_shard_close(st_plan* plan, void* dptr, int opened);
+int st_shard_reset(st_plan* plan, void* buf0);
+int st_solve_sharded(st_plan* plan, int G, int rank, void* const* bufs, const double* c0, const double* b_eq,
+                     const double* geom, int switch_every, int max_iters, double tol, double* c_out,
+                     double* hist, int* iters, int* converged, float* timings_ms);
+
 /* Launch configuration st_solve would use: out[0..7] = cluster size C,
  * agent blocks NB, lane segment width W, threads per CTA, lambda-in-smem flag,
  * dynamic smem bytes, clusters launched, steps per warp task. */

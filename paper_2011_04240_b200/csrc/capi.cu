@@ -55,6 +55,7 @@ struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
   int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_smem_groups = 0;
+  int G = 1;  // groups (GPUs) sharing the scenario; participants = G x K clusters
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -106,7 +107,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   swarm::KParams& k = L.kp;
   const int NP = L.NB * 32, n = pl->n, NW = L.NT / 32, TPW = 32 / L.W;
   L.C = C;
-  const int KC = L.K * C;  // CTAs sharing one scenario
+  const int KC = L.G * L.K * C;  // CTAs sharing one scenario
   L.tmax = ceil_div(pl->m, KC);
   L.tasks_max = ceil_div(L.tmax, TPW);  // time groups of the largest CTA
   // A CTA owns floor(m/C) or ceil(m/C) samples; its warps split groups x steps evenly
@@ -163,7 +164,7 @@ const KernelEntry* find_kernel(int NB, int NVMAX, int LAM) {
   return nullptr;
 }
 
-int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
+int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G = 1) {
   const int n = pl->n;
   if (n < 1 || n > 256) return fail(ST_EUNSUPPORTED, "n_agents must be in [1, 256] for the compiled kernels");
   const int nb_need = n <= 32 ? 1 : ceil_div(n, 32);
@@ -255,10 +256,11 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
       T.nclusters = std::min(batch, active);
       // one large scenario: spread it over every co-resident cluster (grid barrier per iteration)
       const char* mc = std::getenv("SWARM_MULTI_CLUSTER");
-      const bool multi = batch == 1 && C > 1 && active > 1 && (mc ? std::atoi(mc) != 0 : pl->n > 32);
+      const bool multi = G > 1 || (batch == 1 && C > 1 && active > 1 && (mc ? std::atoi(mc) != 0 : pl->n > 32));
       if (multi) {
         Launch M = T;
-        M.K = std::min(active, std::max(1, pl->m / C));
+        M.G = G;
+        M.K = std::min(active, std::max(1, pl->m / (G * C)));
         const long long mbase = layout(pl, M, C);
         long long mneed = mbase + (pass == 0 ? M.lam_per_cta : 0);
         M.lam_smem_groups = 0;
@@ -281,9 +283,14 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L) {
   return fail(ST_EUNSUPPORTED, "no cluster configuration fits this problem on the device");
 }
 
+struct ShardExt {
+  int G, rank;
+  void* bufs[8];
+};
+
 int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double* beq, const double* geom,
         int switch_every, int max_iters, double tol, int flags, double* c_out, double* hist, int* iters,
-        int* conv, double* lam_out, double* d_out, cudaStream_t s) {
+        int* conv, double* lam_out, double* d_out, cudaStream_t s, const ShardExt* ext = nullptr) {
   Launch L = L0;
   swarm::KParams& k = L.kp;
   k.n = pl->n; k.nobs = pl->nobs; k.m = pl->m; k.nv = pl->nv; k.S = pl->S;
@@ -297,10 +304,29 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
   k.switch_every = switch_every; k.max_iters = max_iters; k.flags = flags; k.tol = tol;
   k.K = L.K;
+  k.ngrp = 1;
+  k.g_rank = 0;
+  k.sys_scope = 0;
   k.Rg = nullptr;
   k.gbar = nullptr;
-  if (L.K > 1) {
-    const size_t need = 2 * (size_t)L.K * (3 * (size_t)pl->n * L.NVMAX + 3 * L.NVMAX + 4) * sizeof(double) + 64;
+  for (auto& g : k.Rg_grp) g = nullptr;
+  if (ext != nullptr) {
+    // pair-sharded launch: this GPU is group ext->rank of ext->G; buffers are peer-mapped
+    k.ngrp = ext->G;
+    k.g_rank = ext->rank;
+    k.sys_scope = 1;
+    for (int g = 0; g < ext->G; ++g)
+      k.Rg_grp[g] = reinterpret_cast<double*>(reinterpret_cast<char*>(ext->bufs[g]) + 64);
+    k.gbar = reinterpret_cast<unsigned*>(ext->bufs[0]);
+    k.Rg = k.Rg_grp[0];
+  } else if (L.K > 1) {
+    // one GPU; SWARM_VIRTUAL_GROUPS=g splits the K clusters into g groups with separate buffers
+    // (same participants, same order: bitwise-identical results; exercises the sharded indexing)
+    int gv = 1;
+    if (const char* vg = std::getenv("SWARM_VIRTUAL_GROUPS")) gv = std::max(1, std::atoi(vg));
+    if (gv > 8 || L.K % gv != 0) gv = 1;
+    const size_t per = 2 * (size_t)(L.K / gv) * (3 * (size_t)pl->n * L.NVMAX + 3 * L.NVMAX + 4);
+    const size_t need = gv * per * sizeof(double) + 64;
     if (need > pl->rg_bytes) {
       if (pl->d_rg) cudaFree(pl->d_rg);
       pl->d_rg = nullptr;
@@ -308,8 +334,12 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       ST_CUDA(cudaMalloc(&pl->d_rg, need));
       pl->rg_bytes = need;
     }
+    k.ngrp = gv;
+    k.K = L.K / gv;
     k.gbar = reinterpret_cast<unsigned*>(pl->d_rg);
-    k.Rg = reinterpret_cast<double*>(reinterpret_cast<char*>(pl->d_rg) + 64);
+    for (int g = 0; g < gv; ++g)
+      k.Rg_grp[g] = reinterpret_cast<double*>(reinterpret_cast<char*>(pl->d_rg) + 64) + g * per;
+    k.Rg = k.Rg_grp[0];
     ST_CUDA(cudaMemsetAsync(pl->d_rg, 0, 64, s));
   }
   k.c_global = L.c_global;
@@ -569,9 +599,9 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
              d_out, s);
 }
 
-int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom, int switch_every,
+static int solve_host(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom, int switch_every,
              int max_iters, double tol, int flags, int hint, double* c_out, double* hist, int* iters, int* conv,
-             double* lam_out, double* d_out, float* timings) {
+             double* lam_out, double* d_out, float* timings, const ShardExt* ext) {
   int rc = check_common(pl, batch, switch_every, max_iters, tol, flags);
   if (rc) return rc;
   if (!c0 || !beq || !geom || !c_out || !hist || !iters || !conv) return fail(ST_EINVAL, "NULL buffer");
@@ -580,7 +610,7 @@ int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const 
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L);
+  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, ext ? ext->G : 1);
   if (rc) return rc;
   const int n = pl->n, nv = pl->nv, m = pl->m;
   const long long p = (long long)n * (n - 1) / 2 + (long long)n * pl->nobs;
@@ -609,7 +639,7 @@ int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const 
   ST_CUDA(cudaMemcpyAsync(d_geom, geom, n_g * 8, cudaMemcpyHostToDevice, s));
   ST_CUDA(cudaEventRecord(pl->ev[1], s));
   rc = run(pl, L, batch, d_c0, d_beq, d_geom, switch_every, max_iters, tol, flags, d_cout, d_hist, d_it, d_cv,
-           keep ? d_lam : nullptr, keep ? d_dd : nullptr, s);
+           keep ? d_lam : nullptr, keep ? d_dd : nullptr, s, ext);
   if (rc) return rc;
   ST_CUDA(cudaEventRecord(pl->ev[2], s));
   ST_CUDA(cudaMemcpyAsync(c_out, d_cout, n_c * 8, cudaMemcpyDeviceToHost, s));
@@ -629,6 +659,80 @@ int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const 
     ST_CUDA(cudaEventElapsedTime(&timings[2], pl->ev[2], pl->ev[3]));
   }
   return ST_OK;
+}
+
+int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom, int switch_every,
+             int max_iters, double tol, int flags, int hint, double* c_out, double* hist, int* iters, int* conv,
+             double* lam_out, double* d_out, float* timings) {
+  return solve_host(pl, batch, c0, beq, geom, switch_every, max_iters, tol, flags, hint, c_out, hist, iters, conv,
+                    lam_out, d_out, timings, nullptr);
+}
+
+// ---- pair-sharded solves over G GPUs (one process per GPU, peer-mapped group buffers)
+
+int st_shard_layout(st_plan* pl, int G, long long* out4) {
+  if (!pl || !out4 || G < 1 || G > 8) return fail(ST_EINVAL, "bad arguments (G must be 1..8)");
+  std::lock_guard<std::mutex> g(pl->mu);
+  ST_CUDA(cudaSetDevice(pl->device));
+  Launch L;
+  int rc = choose_launch(pl, 1, 0, false, L, G);
+  if (rc) return rc;
+  const long long stride = 3LL * pl->n * L.NVMAX + 3LL * L.NVMAX + 4;
+  out4[0] = L.C;
+  out4[1] = L.K;
+  out4[2] = 64 + 2LL * L.K * stride * (long long)sizeof(double);
+  out4[3] = (long long)L.G * L.K;
+  return ST_OK;
+}
+
+int st_shard_buffer(st_plan* pl, long long bytes, void** dptr, unsigned char* handle64) {
+  if (!pl || !dptr || !handle64 || bytes < 64) return fail(ST_EINVAL, "bad arguments");
+  ST_CUDA(cudaSetDevice(pl->device));
+  ST_CUDA(cudaMalloc(dptr, (size_t)bytes));
+  ST_CUDA(cudaMemset(*dptr, 0, (size_t)bytes));
+  cudaIpcMemHandle_t h;
+  ST_CUDA(cudaIpcGetMemHandle(&h, *dptr));
+  std::memcpy(handle64, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+  return ST_OK;
+}
+
+int st_shard_open(st_plan* pl, const unsigned char* handle64, void** dptr) {
+  if (!pl || !dptr || !handle64) return fail(ST_EINVAL, "bad arguments");
+  ST_CUDA(cudaSetDevice(pl->device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  ST_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ST_OK;
+}
+
+int st_shard_close(st_plan* pl, void* dptr, int opened) {
+  if (!pl || !dptr) return ST_OK;
+  cudaSetDevice(pl->device);
+  if (opened) cudaIpcCloseMemHandle(dptr);
+  else cudaFree(dptr);
+  return ST_OK;
+}
+
+int st_shard_reset(st_plan* pl, void* buf0) {
+  if (!pl || !buf0) return fail(ST_EINVAL, "bad arguments");
+  ST_CUDA(cudaSetDevice(pl->device));
+  ST_CUDA(cudaMemset(buf0, 0, 64));
+  ST_CUDA(cudaDeviceSynchronize());
+  return ST_OK;
+}
+
+int st_solve_sharded(st_plan* pl, int G, int rank, void* const* bufs, const double* c0, const double* beq,
+                     const double* geom, int switch_every, int max_iters, double tol, double* c_out, double* hist,
+                     int* iters, int* conv, float* timings) {
+  if (!pl || !bufs || G < 1 || G > 8 || rank < 0 || rank >= G) return fail(ST_EINVAL, "bad shard arguments");
+  ShardExt ext;
+  ext.G = G;
+  ext.rank = rank;
+  for (int g = 0; g < 8; ++g) ext.bufs[g] = g < G ? bufs[g] : nullptr;
+  for (int g = 0; g < G; ++g)
+    if (!ext.bufs[g]) return fail(ST_EINVAL, "NULL group buffer");
+  return solve_host(pl, 1, c0, beq, geom, switch_every, max_iters, tol, 0, 0, c_out, hist, iters, conv, nullptr,
+                    nullptr, timings, &ext);
 }
 
 }  // extern "C"

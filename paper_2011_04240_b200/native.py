@@ -21,7 +21,8 @@ ST_FLAG_KEEP_STATE = 1
 _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedError}
 
 EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
-           "st_last_error", "st_version")
+           "st_last_error", "st_version", "st_shard_layout", "st_shard_buffer", "st_shard_open", "st_shard_close",
+           "st_shard_reset", "st_solve_sharded")
 
 _lib = None
 _lock = threading.Lock()
@@ -49,6 +50,14 @@ def load() -> ctypes.CDLL:
         lib.st_solve_device.argtypes = [vp, i, vp, vp, vp, i, i, d, i, i, vp, vp, vp, vp, vp, vp, vp]
         lib.st_query_launch.argtypes = [vp, i, i, ctypes.POINTER(ctypes.c_longlong)]
         lib.st_last_error.restype = ctypes.c_char_p
+        ub = ctypes.POINTER(ctypes.c_ubyte)
+        lib.st_shard_layout.argtypes = [vp, i, ctypes.POINTER(ctypes.c_longlong)]
+        lib.st_shard_buffer.argtypes = [vp, ctypes.c_longlong, ctypes.POINTER(vp), ub]
+        lib.st_shard_open.argtypes = [vp, ub, ctypes.POINTER(vp)]
+        lib.st_shard_close.argtypes = [vp, vp, i]
+        lib.st_shard_reset.argtypes = [vp, vp]
+        lib.st_solve_sharded.argtypes = [vp, i, i, ctypes.POINTER(vp), _dp, _dp, _dp, i, i, d, _dp, _dp, _ip, _ip,
+                                         ctypes.POINTER(ctypes.c_float)]
         for name in EXPORTS:
             getattr(lib, name)  # every declared symbol must resolve
         _lib = lib
@@ -142,3 +151,46 @@ class Plan:
         _check(self._lib.st_solve_device(self._h, B, c0_ptr, beq_ptr, geom_ptr, switch_every, max_iters, tol,
                                          0, cluster_hint, c_out_ptr, hist_ptr, iters_ptr, conv_ptr, None, None,
                                          stream or None))
+
+    # ---- pair sharding over GPUs (one process per GPU; see include/swarm_am.h) -------------
+
+    def shard_layout(self, groups: int) -> dict:
+        out = (ctypes.c_longlong * 4)()
+        _check(self._lib.st_shard_layout(self._h, groups, out))
+        return {"cluster": int(out[0]), "clusters_per_gpu": int(out[1]), "buffer_bytes": int(out[2]),
+                "participants": int(out[3])}
+
+    def shard_buffer(self, nbytes: int) -> tuple[int, bytes]:
+        ptr = ctypes.c_void_p()
+        h = (ctypes.c_ubyte * 64)()
+        _check(self._lib.st_shard_buffer(self._h, nbytes, ctypes.byref(ptr), h))
+        return ptr.value, bytes(h)
+
+    def shard_open(self, handle: bytes) -> int:
+        ptr = ctypes.c_void_p()
+        h = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+        _check(self._lib.st_shard_open(self._h, h, ctypes.byref(ptr)))
+        return ptr.value
+
+    def shard_close(self, ptr: int, opened: bool) -> None:
+        self._lib.st_shard_close(self._h, ptr, 1 if opened else 0)
+
+    def shard_reset(self, buf0: int) -> None:
+        _check(self._lib.st_shard_reset(self._h, buf0))
+
+    def solve_sharded(self, groups: int, rank: int, bufs, c0, beq, geom, switch_every: int, max_iters: int,
+                      tol: float) -> dict:
+        c0 = np.ascontiguousarray(c0, dtype=np.float64)
+        beq = np.ascontiguousarray(beq, dtype=np.float64)
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        c_out = np.empty_like(c0)
+        hist = np.empty((1, 3, max_iters))
+        iters = np.empty(1, dtype=np.int32)
+        conv = np.empty(1, dtype=np.int32)
+        arr = (ctypes.c_void_p * groups)(*bufs)
+        t = (ctypes.c_float * 3)()
+        _check(self._lib.st_solve_sharded(self._h, groups, rank, arr, _ptr(c0), _ptr(beq), _ptr(geom), switch_every,
+                                          max_iters, tol, _ptr(c_out), _ptr(hist), _ptr(iters, _ip), _ptr(conv, _ip),
+                                          t))
+        return {"c": c_out, "hist": hist, "iters": iters, "converged": conv.astype(bool),
+                "timings_ms": tuple(float(x) for x in t)}

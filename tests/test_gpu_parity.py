@@ -159,3 +159,17 @@ def test_results_independent_of_stale_device_memory(cuda_ok, name):
     rep = am_solve(spec, _config(cfg), cache=FactorCache())
     assert rep.iterations == int(ref["iterations"])
     assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref)
+
+
+@pytest.mark.parametrize("name,groups", [("rand256_s0", 2), ("rand256_s0", 3), ("sph64j", 2)])
+def test_virtual_groups_reproduce_multi_cluster_bitwise(cuda_ok, name, groups, monkeypatch):
+    """The pair-sharded exchange (participants in per-group buffers, fixed participant order)
+    run as `groups` virtual groups on one GPU must equal the single-group multi-cluster solve."""
+    from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve
+    spec, cfg, ref = load_golden(name)
+    base = am_solve(spec, SolverConfig(max_iters=40), cache=FactorCache())
+    monkeypatch.setenv("SWARM_VIRTUAL_GROUPS", str(groups))
+    rep = am_solve(spec, SolverConfig(max_iters=40), cache=FactorCache())
+    assert rep.iterations == base.iterations
+    np.testing.assert_array_equal(rep.coefficients, base.coefficients)
+    np.testing.assert_array_equal(rep.residual_max_history, base.residual_max_history)
