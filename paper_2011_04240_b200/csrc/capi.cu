@@ -213,7 +213,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam);
     if (!ke) continue;
     {
-      if (C > pl->m || C < 1 || C > 16) continue;
+      if ((long long)C * G > pl->m || C < 1 || C > 16) continue;  // every CTA owns >= 1 sample
       Launch T = L;
       T.NT = ke->NT;
       T.fn = ke->fn;

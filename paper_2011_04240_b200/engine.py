@@ -203,38 +203,11 @@ def _alpha_beta(diffs, l_xy, l_z):
     return alpha, beta
 
 
-def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorCache | None = None,
-                   with_metrics: bool = True) -> list:
-    """Solve scenarios sharing one fingerprint in one device launch; one report each."""
-    config = config or SolverConfig()
-    specs = list(specs)
-    if not specs:
-        return []
-    if config.track_descent:
-        raise NotImplementedError("track_descent (an augmented-cost diagnostic between axis solves) is not "
-                                  "implemented by the device loop")
-    for spec in specs:
-        v = validate(spec)
-        if v:
-            raise InfeasibleProblemError(v)
-    _check_batch(specs)
-    if config.keep_state and len(specs) != 1:
-        raise ValueError("keep_state is only available for single solves")
-    t0 = time.perf_counter()
-    spec0 = specs[0]
-    n, n_obs = len(spec0.start), len(spec0.obstacles)
-    basis = poly.for_spec(spec0)
-    fp = kkt.fingerprint(basis, n, n_obs)
-    c0, beq, geom = pack(specs, basis)
-    t1 = time.perf_counter()
-    cache = cache if cache is not None else default_cache()
-    schedule = config.schedule()
-    plan = _plan_for(cache, fp, basis, schedule, n, n_obs, config.device)
-    t2 = time.perf_counter()
-    out = plan.solve(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
-                     keep_state=config.keep_state, cluster_hint=config.cluster_size)
-    t3 = time.perf_counter()
+def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with_metrics=True) -> list:
+    """Device outputs of one launch -> one SolveReport per scenario (reference field layout)."""
+    t0, t1, t2, t3 = stamps
     h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
+    n, n_obs = len(specs[0].start), len(specs[0].obstacles)
     reports = []
     for b, spec in enumerate(specs):
         it = int(out["iters"][b])
@@ -294,7 +267,42 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
             cache_stats=cache.stats(),
             diagnostics=diagnostics,
         ))
-    log.info("batch of %d solved on device in %.3f ms", len(specs), loop_ms)
+    return reports
+
+
+def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorCache | None = None,
+                   with_metrics: bool = True) -> list:
+    """Solve scenarios sharing one fingerprint in one device launch; one report each."""
+    config = config or SolverConfig()
+    specs = list(specs)
+    if not specs:
+        return []
+    if config.track_descent:
+        raise NotImplementedError("track_descent (an augmented-cost diagnostic between axis solves) is not "
+                                  "implemented by the device loop")
+    for spec in specs:
+        v = validate(spec)
+        if v:
+            raise InfeasibleProblemError(v)
+    _check_batch(specs)
+    if config.keep_state and len(specs) != 1:
+        raise ValueError("keep_state is only available for single solves")
+    t0 = time.perf_counter()
+    spec0 = specs[0]
+    n, n_obs = len(spec0.start), len(spec0.obstacles)
+    basis = poly.for_spec(spec0)
+    fp = kkt.fingerprint(basis, n, n_obs)
+    c0, beq, geom = pack(specs, basis)
+    t1 = time.perf_counter()
+    cache = cache if cache is not None else default_cache()
+    schedule = config.schedule()
+    plan = _plan_for(cache, fp, basis, schedule, n, n_obs, config.device)
+    t2 = time.perf_counter()
+    out = plan.solve(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
+                     keep_state=config.keep_state, cluster_hint=config.cluster_size)
+    t3 = time.perf_counter()
+    reports = _make_reports(specs, out, basis, plan, cache, schedule, config, (t0, t1, t2, t3), with_metrics)
+    log.info("batch of %d solved on device in %.3f ms", len(specs), out["timings_ms"][1])
     return reports
 
 

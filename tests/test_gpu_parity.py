@@ -173,3 +173,32 @@ def test_virtual_groups_reproduce_multi_cluster_bitwise(cuda_ok, name, groups, m
     assert rep.iterations == base.iterations
     np.testing.assert_array_equal(rep.coefficients, base.coefficients)
     np.testing.assert_array_equal(rep.residual_max_history, base.residual_max_history)
+
+
+@pytest.mark.parametrize("name", ["rand128_s0", "circ16j"])
+def test_pair_sharded_entry_single_rank_matches_am_solve(cuda_ok, name):
+    """am_solve_pair_sharded end to end (IPC buffer export, barrier reset, sharded launch) on a
+    one-rank group: bitwise equal to am_solve (multi-GPU runs differ only in the group count,
+    which the virtual-group test covers on one device)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve
+    from paper_2011_04240_b200.dist import am_solve_pair_sharded
+    spec, cfg, ref = load_golden(name)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        cache = FactorCache()
+        base = am_solve(spec, SolverConfig(max_iters=60), cache=cache)
+        rep = am_solve_pair_sharded(spec, SolverConfig(max_iters=60), cache=cache)
+        rep2 = am_solve_pair_sharded(spec, SolverConfig(max_iters=60), cache=cache)  # buffers reused cleanly
+    finally:
+        dist.destroy_process_group()
+    assert rep.iterations == base.iterations == rep2.iterations
+    np.testing.assert_array_equal(rep.coefficients, base.coefficients)
+    np.testing.assert_array_equal(rep2.coefficients, base.coefficients)
+    np.testing.assert_array_equal(rep.residual_norm_history, base.residual_norm_history)
