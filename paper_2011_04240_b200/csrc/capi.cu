@@ -36,6 +36,7 @@ using KernelFn = void (*)(swarm::KParams);
 struct KernelEntry {
   int NB, NT, NVMAX, LAM;
   KernelFn fn;
+  int minb = 1;  // CTAs per SM the kernel is register-bounded for
 };
 
 using swarm::am_cluster_kernel;
@@ -49,6 +50,8 @@ const KernelEntry kKernels[] = {
     {2, 384, 16, kG, am_cluster_kernel<2, 384, 16, kG>}, {2, 384, 16, kK, am_cluster_kernel<2, 384, 16, kK>},
     {4, 256, 12, kG, am_cluster_kernel<4, 256, 12, kG>}, {4, 256, 12, kK, am_cluster_kernel<4, 256, 12, kK>},
     {8, 256, 12, kG, am_cluster_kernel<8, 256, 12, kG>}, {8, 256, 12, kK, am_cluster_kernel<8, 256, 12, kK>},
+    // two CTAs per SM (batches of small fleets): independent scenarios hide each other's exchange latency
+    {1, 256, 12, kG, am_cluster_kernel<1, 256, 12, kG, 2>, 2}, {1, 256, 16, kG, am_cluster_kernel<1, 256, 16, kG, 2>, 2},
 };
 
 struct Launch {
@@ -80,6 +83,7 @@ struct st_plan {
   void* d_io = nullptr;  // inputs+outputs of host-pointer solves
   size_t io_bytes = 0;
   int smem_optin = 0;
+  int smem_sm = 0;  // shared memory per SM
   std::mutex mu;
 };
 
@@ -129,12 +133,12 @@ long long layout(st_plan* pl, Launch& L, int C) {
   const int NV = L.NVMAX;
   take(k.o_c, L.c_global ? 0 : 3LL * n * NV);
   // Regions never live at the same time share storage:
-  //   qp (pairwise -> combine)  and  Rp (projection -> owners' pull, before the next pairwise)
+  //   qp (pairwise -> combine) and Rp (projection -> owners' pull, before the next pairwise)
+  //   X (positions -> pairwise) and qc (combine -> projection)
   const long long qp_sz = (long long)NW * L.qslots * 3 * NP, rp_sz = 3LL * n * NV;
   take(k.o_qp, std::max(qp_sz, rp_sz));
   k.o_Rp = k.o_qp;
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
-  //   X (positions -> pairwise)  and  qc (combine -> projection)
   const long long x_sz = (long long)L.tasks_max * 3 * NP, qc_sz = (long long)L.tmax * 3 * n + 3LL * L.tmax;
   take(k.o_X, std::max(x_sz, qc_sz));
   k.o_qc = k.o_X;
@@ -158,9 +162,9 @@ long long layout(st_plan* pl, Launch& L, int C) {
   return o;
 }
 
-const KernelEntry* find_kernel(int NB, int NVMAX, int LAM) {
+const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, int minb = 1) {
   for (const auto& e : kKernels)
-    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM) return &e;
+    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM && e.minb == minb) return &e;
   return nullptr;
 }
 
@@ -210,8 +214,13 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     if (cg_try == 1 && pass == 0) continue;  // coefficients in global memory only with lambda there too
     const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
     if (keep && pass == 0) continue;
-    const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam);
+    // batches with lambda in L2: two CTAs (two scenarios) per SM when the dual kernel exists
+    const char* du = std::getenv("SWARM_DUAL");
+    const bool dual = throughput && pass == 1 && !keep && (du ? std::atoi(du) != 0 : false);
+    const KernelEntry* ke = dual ? find_kernel(NB, pl->nvmax, lam, 2) : nullptr;
+    if (!ke) ke = find_kernel(NB, pl->nvmax, lam);
     if (!ke) continue;
+    const long long bud = ke->minb == 2 ? (pl->smem_sm / 2 - 1024) / 8 : budget;
     {
       if ((long long)C * G > pl->m || C < 1 || C > 16) continue;  // every CTA owns >= 1 sample
       Launch T = L;
@@ -220,7 +229,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       T.c_global = cg_try;
       const long long base = layout(pl, T, C);
       const long long need = base + (pass == 0 ? T.lam_per_cta : 0);
-      if (need > budget) continue;
+      if (need > bud) continue;
       T.lam_smem = pass == 0 ? 1 : 0;
       T.lam_smem_groups = 0;
       long long need2 = need;
@@ -229,7 +238,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
         const long long per_group = (long long)T.nsteps * 96;
         const char* hy = std::getenv("SWARM_LAM_HYBRID");
         if (!hy || std::atoi(hy) != 0) {
-          T.lam_smem_groups = (int)std::min<long long>(T.tasks_max, (budget - need) / per_group);
+          T.lam_smem_groups = (int)std::min<long long>(T.tasks_max, (bud - need) / per_group);
           need2 = need + (long long)T.lam_smem_groups * per_group;
         }
       }
@@ -429,7 +438,16 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
     if (cnt) {
       std::fprintf(stderr, "[swarm timers] C=%d NB=%d iters=%d cycles/iter:", L.C, L.NB, cnt);
       for (int q = 0; q < 9; ++q) std::fprintf(stderr, " %s=%.0f", names[q], acc[q] / cnt);
-      std::fprintf(stderr, "\n");
+      double sub[3] = {0, 0, 0}, drain = 0;
+      for (int it = 1; it <= cnt; ++it) {
+        const long long* t = &h[16 * it];
+        sub[0] += t[9] - t[11];
+        drain += t[11] - t[7];
+        sub[1] += t[10] - t[9];
+        sub[2] += t[8] - t[10];
+      }
+      std::fprintf(stderr, " [project: drain=%.0f combine=%.0f sync=%.0f basis=%.0f]\n", drain / cnt, sub[0] / cnt,
+                   sub[1] / cnt, sub[2] / cnt);
     }
   }
   return 0;
@@ -535,6 +553,7 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&pl->ev[i]);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   if (e != cudaSuccess) {
     fail(e == cudaErrorMemoryAllocation ? ST_ENOMEM : ST_ECUDA, std::string("plan upload: ") + cudaGetErrorString(e));
     return cleanup(e == cudaErrorMemoryAllocation ? ST_ENOMEM : ST_ECUDA);

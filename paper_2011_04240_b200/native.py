@@ -15,7 +15,8 @@ import numpy as np
 
 from . import poly
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_swarm_am.so")
+# SWARM_LIB: alternative build of the same library (A/B comparisons of kernel changes)
+LIB_PATH = os.environ.get("SWARM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_swarm_am.so")
 
 ST_FLAG_KEEP_STATE = 1
 _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedError}
