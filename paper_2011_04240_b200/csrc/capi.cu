@@ -40,7 +40,7 @@ struct KernelEntry {
 };
 
 using swarm::am_cluster_kernel;
-constexpr int kS = swarm::LAM_SMEM, kG = swarm::LAM_GLOBAL, kK = swarm::LAM_GLOBAL_KEEP;
+constexpr int kS = swarm::LAM_SMEM, kG = swarm::LAM_GLOBAL, kK = swarm::LAM_GLOBAL_KEEP, kT = swarm::LAM_STREAM;
 // lambda fits in shared memory only for n <= 32 (NB == 1); larger fleets stream it from L2.
 const KernelEntry kKernels[] = {
     {1, 512, 12, kS, am_cluster_kernel<1, 512, 12, kS>}, {1, 512, 12, kG, am_cluster_kernel<1, 512, 12, kG>},
@@ -50,6 +50,10 @@ const KernelEntry kKernels[] = {
     {2, 384, 16, kG, am_cluster_kernel<2, 384, 16, kG>}, {2, 384, 16, kK, am_cluster_kernel<2, 384, 16, kK>},
     {4, 256, 12, kG, am_cluster_kernel<4, 256, 12, kG>}, {4, 256, 12, kK, am_cluster_kernel<4, 256, 12, kK>},
     {8, 256, 12, kG, am_cluster_kernel<8, 256, 12, kG>}, {8, 256, 12, kK, am_cluster_kernel<8, 256, 12, kK>},
+    // multipliers streamed through shared memory by TMA bulk copies (LAM_STREAM)
+    {1, 512, 12, kT, am_cluster_kernel<1, 512, 12, kT>}, {1, 512, 16, kT, am_cluster_kernel<1, 512, 16, kT>},
+    {2, 384, 12, kT, am_cluster_kernel<2, 384, 12, kT>}, {2, 384, 16, kT, am_cluster_kernel<2, 384, 16, kT>},
+    {4, 256, 12, kT, am_cluster_kernel<4, 256, 12, kT>}, {8, 256, 12, kT, am_cluster_kernel<8, 256, 12, kT>},
     // two CTAs per SM (batches of small fleets): independent scenarios hide each other's exchange latency
     {1, 256, 12, kG, am_cluster_kernel<1, 256, 12, kG, 2>, 2}, {1, 256, 16, kG, am_cluster_kernel<1, 256, 16, kG, 2>, 2},
 };
@@ -57,8 +61,9 @@ const KernelEntry kKernels[] = {
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_smem_groups = 0;
+  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_tail = 0;
   int G = 1;  // groups (GPUs) sharing the scenario; participants = G x K clusters
+  int stream = 0;  // LAM_STREAM: per-warp TMA rings for the multipliers
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -139,7 +144,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_qp, std::max(qp_sz, rp_sz));
   k.o_Rp = k.o_qp;
   take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
-  const long long x_sz = (long long)L.tasks_max * 3 * NP, qc_sz = (long long)L.tmax * 3 * n + 3LL * L.tmax;
+  const long long x_sz = (long long)L.tasks_max * 3 * NP, qc_sz = (long long)L.tmax * ((3LL * n + 1) & ~1LL) + 3LL * L.tmax;
   take(k.o_X, std::max(x_sz, qc_sz));
   k.o_qc = k.o_X;
   take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
@@ -157,9 +162,19 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_bb, 18);
   take(k.o_wp, 2LL * NW);
   take(k.o_misc, 2);
+  take(k.o_ring, L.stream ? (long long)NW * swarm::LS_R * swarm::LS_K * 96 : 0);
+  take(k.o_mbar, L.stream ? (long long)NW * (swarm::LS_R + 1) : 0);
   k.o_lam = (int)o;
   L.lam_per_cta = (long long)L.tasks_max * L.nsteps * 96;
   return o;
+}
+
+// Hybrid multipliers: rows per warp kept in shared memory (each warp's last rows), from
+// `spare` doubles of shared memory, at most the rows of the longest warp range.
+int tail_rows(const Launch& L, long long spare) {
+  const int NW = L.NT / 32, TPW = 32 / L.W;
+  const long long rows_max = ceil_div((long long)ceil_div(L.tmax, TPW) * L.nsteps, NW);
+  return (int)std::max(0LL, std::min(rows_max, spare / (96LL * NW)));
 }
 
 const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, int minb = 1) {
@@ -212,7 +227,10 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
   for (const auto& cp : order) {
     const int C = cp.first, pass = cp.second;
     if (cg_try == 1 && pass == 0) continue;  // coefficients in global memory only with lambda there too
-    const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
+    const char* lst = std::getenv("SWARM_LAM_STREAM");
+    const bool stream = lst ? std::atoi(lst) != 0 : false;
+    const int lam = pass == 0 ? swarm::LAM_SMEM
+                              : (keep ? swarm::LAM_GLOBAL_KEEP : (stream ? swarm::LAM_STREAM : swarm::LAM_GLOBAL));
     if (keep && pass == 0) continue;
     // batches with lambda in L2: two CTAs (two scenarios) per SM when the dual kernel exists
     const char* du = std::getenv("SWARM_DUAL");
@@ -227,19 +245,19 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       T.NT = ke->NT;
       T.fn = ke->fn;
       T.c_global = cg_try;
+      T.stream = lam == swarm::LAM_STREAM ? 1 : 0;
       const long long base = layout(pl, T, C);
       const long long need = base + (pass == 0 ? T.lam_per_cta : 0);
       if (need > bud) continue;
       T.lam_smem = pass == 0 ? 1 : 0;
-      T.lam_smem_groups = 0;
+      T.lam_tail = 0;
       long long need2 = need;
-      if (pass == 1 && !keep) {
+      if (pass == 1 && !keep && !T.stream) {
         // hybrid: spare shared memory holds the first groups of lambda (the rest stays in L2)
-        const long long per_group = (long long)T.nsteps * 96;
         const char* hy = std::getenv("SWARM_LAM_HYBRID");
         if (!hy || std::atoi(hy) != 0) {
-          T.lam_smem_groups = (int)std::min<long long>(T.tasks_max, (bud - need) / per_group);
-          need2 = need + (long long)T.lam_smem_groups * per_group;
+          T.lam_tail = tail_rows(T, bud - need);
+          need2 = need + (long long)T.lam_tail * 96 * (T.NT / 32);
         }
       }
       T.smem_bytes = (size_t)need2 * 8;
@@ -272,11 +290,10 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
         M.K = std::min(active, std::max(1, pl->m / (G * C)));
         const long long mbase = layout(pl, M, C);
         long long mneed = mbase + (pass == 0 ? M.lam_per_cta : 0);
-        M.lam_smem_groups = 0;
-        if (pass == 1 && !keep && mneed <= budget) {
-          const long long per_group = (long long)M.nsteps * 96;
-          M.lam_smem_groups = (int)std::min<long long>(M.tasks_max, (budget - mneed) / per_group);
-          mneed += (long long)M.lam_smem_groups * per_group;
+        M.lam_tail = 0;
+        if (pass == 1 && !keep && !M.stream && mneed <= budget) {
+          M.lam_tail = tail_rows(M, budget - mneed);
+          mneed += (long long)M.lam_tail * 96 * (M.NT / 32);
         }
         if (mneed <= budget) {
           M.smem_bytes = (size_t)mneed * 8;
@@ -307,7 +324,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.mats = pl->mats; k.inv_rho = pl->inv_rho;
   k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
   k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots; k.wpg = L.wpg;
-  k.lam_smem_groups = L.lam_smem_groups;
+  k.lam_tail = L.lam_tail;
   k.B = batch; k.gstride = 2 + 5 * pl->nobs;
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
   k.lam_out = lam_out; k.d_out = d_out; k.counter = pl->d_counter;
@@ -382,7 +399,9 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
       cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
       const size_t used = (size_t)L.nclusters * L.C * L.lam_per_cta * sizeof(double);
-      const double gfrac = L.tasks_max > 0 ? 1.0 - (double)L.lam_smem_groups / L.tasks_max : 1.0;
+      const int TPWl = 32 / L.W, NWl = L.NT / 32;
+      const long long rows_w = ceil_div((long long)ceil_div(L.tmax, TPWl) * L.nsteps, NWl);
+      const double gfrac = rows_w > 0 ? 1.0 - (double)L.lam_tail / rows_w : 1.0;
       if (max_persist > 0 && max_window > 0) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
         cudaStreamAttrValue av = {};
@@ -395,8 +414,8 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
         cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
         cudaGetLastError();
         if (std::getenv("SWARM_VERBOSE"))
-          std::fprintf(stderr, "[swarm] L2 persisting: max %d B, window max %d B, lambda %zu B, smem groups %d/%d\n",
-                       max_persist, max_window, used, L.lam_smem_groups, L.tasks_max);
+          std::fprintf(stderr, "[swarm] L2 persisting: max %d B, window max %d B, lambda %zu B, smem rows per warp %d/%lld\n",
+                       max_persist, max_window, used, L.lam_tail, rows_w);
       }
     }
   } else {
