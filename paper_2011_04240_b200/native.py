@@ -120,8 +120,12 @@ class Plan:
         return dict(zip(keys, (int(v) for v in out)))
 
     def solve(self, c0, beq, geom, switch_every: int, max_iters: int, tol: float,
-              keep_state: bool = False, cluster_hint: int = 0) -> dict:
-        """Host-buffer solve of a batch: c0 (B,3,n,nv), beq (B,3,n,6), geom (B, 2+5 n_obs)."""
+              keep_state: bool = False, cluster_hint: int = 0, out: dict | None = None) -> dict:
+        """Host-buffer solve of a batch: c0 (B,3,n,nv), beq (B,3,n,6), geom (B, 2+5 n_obs).
+
+        ``out`` may supply preallocated (e.g. page-locked) output arrays: ``c`` (B,3,n,nv)
+        float64, ``hist`` (B,3,max_iters) float64, ``iters`` and ``converged`` (B,) int32.
+        """
         c0 = np.ascontiguousarray(c0, dtype=np.float64)
         beq = np.ascontiguousarray(beq, dtype=np.float64)
         geom = np.ascontiguousarray(geom, dtype=np.float64)
@@ -130,10 +134,17 @@ class Plan:
                 geom.shape != (B, 2 + 5 * self.n_obs):
             raise ValueError(f"batch arrays have shapes {c0.shape}, {beq.shape}, {geom.shape}; expected "
                              f"({B}, 3, {self.n}, {self.nv}), ({B}, 3, {self.n}, 6), ({B}, {2 + 5 * self.n_obs})")
-        c_out = np.empty_like(c0)
-        hist = np.empty((B, 3, max_iters))
-        iters = np.empty(B, dtype=np.int32)
-        conv = np.empty(B, dtype=np.int32)
+        if out is not None:
+            c_out, hist, iters, conv = out["c"], out["hist"], out["iters"], out["converged"]
+            for arr, shape, dt in ((c_out, c0.shape, np.float64), (hist, (B, 3, max_iters), np.float64),
+                                   (iters, (B,), np.int32), (conv, (B,), np.int32)):
+                if arr.shape != shape or arr.dtype != dt or not arr.flags.c_contiguous:
+                    raise ValueError(f"output buffer {arr.shape}/{arr.dtype} does not match {shape}/{dt}")
+        else:
+            c_out = np.empty_like(c0)
+            hist = np.empty((B, 3, max_iters))
+            iters = np.empty(B, dtype=np.int32)
+            conv = np.empty(B, dtype=np.int32)
         lam = d = None
         if keep_state:
             lam = np.empty((3, self.num_pairs, self.m))
@@ -142,8 +153,8 @@ class Plan:
         _check(self._lib.st_solve(self._h, B, _ptr(c0), _ptr(beq), _ptr(geom), switch_every, max_iters, tol,
                                   ST_FLAG_KEEP_STATE if keep_state else 0, cluster_hint, _ptr(c_out),
                                   _ptr(hist), _ptr(iters, _ip), _ptr(conv, _ip), _ptr(lam), _ptr(d), t))
-        return {"c": c_out, "hist": hist, "iters": iters, "converged": conv.astype(bool), "lam": lam, "d": d,
-                "timings_ms": tuple(float(x) for x in t)}
+        return {"c": c_out, "hist": hist, "iters": iters, "converged": conv if out is not None else conv.astype(bool),
+                "lam": lam, "d": d, "timings_ms": tuple(float(x) for x in t)}
 
     def solve_device(self, B: int, c0_ptr: int, beq_ptr: int, geom_ptr: int, switch_every: int,
                      max_iters: int, tol: float, c_out_ptr: int, hist_ptr: int, iters_ptr: int,
