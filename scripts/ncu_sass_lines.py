@@ -20,8 +20,12 @@ for ln in sass.splitlines():
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
     if m and fn and kern in fn:
         a2l[int(m.group(1), 16)] = cur
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".gz"):
+    import gzip
+    out = gzip.open(rep, "rt").read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
 ia, ie, iss, isrc = h.index("Address"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
