@@ -33,8 +33,12 @@ def func_of(f, line):
         if s <= line:
             name = n
     return name
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
-                     text=True).stdout
+if rep.endswith(".gz"):
+    import gzip
+    out = gzip.open(rep, "rt").read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ia, ie, isrc = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Source")
