@@ -15,16 +15,19 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_swarm_am.so")
-SOURCES = [os.path.join(CSRC, "capi.cu")]
+# capi.cu holds the host side; the kernel variants are explicitly instantiated in inst_*.cu
+# so the (independent, slow) device compilations run in parallel
+SOURCES = [os.path.join(CSRC, f) for f in ("capi.cu", "inst_nb1_12.cu", "inst_nb1_16.cu", "inst_nb2.cu",
+                                           "inst_nb48.cu", "inst_experimental.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "am_kernel.cuh"), os.path.join(ROOT, "include", "swarm_am.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
-    "--cudart", "static",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "static"]
 
 
 def nvcc() -> str:
@@ -41,21 +44,38 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
     if not force and not stale():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(CSRC, "obj")
+    os.makedirs(objdir, exist_ok=True)
     log = os.path.join(HERE, "csrc", "build.log")
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra_flags, "-c", "-o", obj, src]
+        return cmd, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    text = ""
+    for cmd, obj, res in results:
+        text += " ".join(cmd) + "\n" + res.stdout + res.stderr
+    tmp = LIB + ".tmp"
+    link = [nvcc(), *LINK_FLAGS, "-o", tmp, *[obj for _, obj, _ in results]]
+    lres = None
+    if all(res.returncode == 0 for _, _, res in results):
+        lres = subprocess.run(link, capture_output=True, text=True)
+        text += " ".join(link) + "\n" + lres.stdout + lres.stderr
     with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed (exit {res.returncode}); see {log}")
+        fh.write(text)
+    if lres is None or lres.returncode != 0:
+        sys.stderr.write(text[-4000:])
+        raise RuntimeError(f"nvcc failed; see {log}")
     os.replace(tmp, LIB)
     if verbose:
-        sys.stdout.write(res.stderr)
+        sys.stdout.write(text)
     return LIB
 
 

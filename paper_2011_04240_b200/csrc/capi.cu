@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/swarm_am.h"
+#define SWARM_KERNEL_DECL_ONLY
 #include "am_kernel.cuh"
 
 namespace {
@@ -50,12 +51,15 @@ const KernelEntry kKernels[] = {
     {2, 384, 16, kG, am_cluster_kernel<2, 384, 16, kG>}, {2, 384, 16, kK, am_cluster_kernel<2, 384, 16, kK>},
     {4, 256, 12, kG, am_cluster_kernel<4, 256, 12, kG>}, {4, 256, 12, kK, am_cluster_kernel<4, 256, 12, kK>},
     {8, 256, 12, kG, am_cluster_kernel<8, 256, 12, kG>}, {8, 256, 12, kK, am_cluster_kernel<8, 256, 12, kK>},
-    // multipliers streamed through shared memory by TMA bulk copies (LAM_STREAM)
+#ifdef SWARM_EXPERIMENTAL_KERNELS
+    // measured slower than the defaults, built only with -DSWARM_EXPERIMENTAL_KERNELS:
+    // multipliers streamed through shared memory by TMA bulk copies (LAM_STREAM, SWARM_LAM_STREAM=1)
     {1, 512, 12, kT, am_cluster_kernel<1, 512, 12, kT>}, {1, 512, 16, kT, am_cluster_kernel<1, 512, 16, kT>},
     {2, 384, 12, kT, am_cluster_kernel<2, 384, 12, kT>}, {2, 384, 16, kT, am_cluster_kernel<2, 384, 16, kT>},
     {4, 256, 12, kT, am_cluster_kernel<4, 256, 12, kT>}, {8, 256, 12, kT, am_cluster_kernel<8, 256, 12, kT>},
-    // two CTAs per SM (batches of small fleets): independent scenarios hide each other's exchange latency
+    // two CTAs per SM (SWARM_DUAL=1)
     {1, 256, 12, kG, am_cluster_kernel<1, 256, 12, kG, 2>, 2}, {1, 256, 16, kG, am_cluster_kernel<1, 256, 16, kG, 2>, 2},
+#endif
 };
 
 struct Launch {
@@ -228,7 +232,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     const int C = cp.first, pass = cp.second;
     if (cg_try == 1 && pass == 0) continue;  // coefficients in global memory only with lambda there too
     const char* lst = std::getenv("SWARM_LAM_STREAM");
-    const bool stream = lst ? std::atoi(lst) != 0 : false;
+    const bool stream = (lst ? std::atoi(lst) != 0 : false) && find_kernel(NB, pl->nvmax, swarm::LAM_STREAM);
     const int lam = pass == 0 ? swarm::LAM_SMEM
                               : (keep ? swarm::LAM_GLOBAL_KEEP : (stream ? swarm::LAM_STREAM : swarm::LAM_GLOBAL));
     if (keep && pass == 0) continue;

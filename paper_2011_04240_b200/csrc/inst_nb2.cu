@@ -1,0 +1,10 @@
+// Explicit instantiations of the AM kernel variants listed in capi.cu (kKernels), split over
+// translation units so that nvcc compiles them in parallel (_build.py).
+#include "am_kernel.cuh"
+
+namespace swarm {
+template __global__ void am_cluster_kernel<2, 384, 12, 1, 1>(const KParams);
+template __global__ void am_cluster_kernel<2, 384, 12, 2, 1>(const KParams);
+template __global__ void am_cluster_kernel<2, 384, 16, 1, 1>(const KParams);
+template __global__ void am_cluster_kernel<2, 384, 16, 2, 1>(const KParams);
+}  // namespace swarm
