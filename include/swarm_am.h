@@ -104,6 +104,21 @@ int st_solve_sharded(st_plan* plan, int G, int rank, void* const* bufs, const do
  * dynamic smem bytes, clusters launched, steps per warp task. */
 int st_query_launch(st_plan* plan, int batch, int cluster_hint, long long* out8);
 
+/* Post-solve safety verdict (replaces validation.py:39-93, check_collisions,
+ * called by _final_metrics, solver.py:497-509).  Host buffers.
+ *   traj   n x m x 3 sampled positions (SolveReport.trajectories)
+ *   obs    n_obs x 5: center x, y, z, l_xy/2 + radius, l_z/2 + radius
+ * Rows in the reference order (agent pairs i<j lexicographic, then agent-major
+ * (agent, obstacle)), samples in order.  Writes min(total, cap) violations:
+ * ids[4e..4e+3] = kind (0 agent pair, 1 obstacle), i, j-or-k, sample;
+ * vals[e] = normalized distance (< 1).  *min_out = global minimum (+inf when
+ * there are no rows), *total_out = number of violations (may exceed cap; call
+ * again with a larger cap for the full list).  Values are bit-identical to
+ * the reference's scalar loop. */
+int st_check_collisions(int n, int m, const double* traj, double l_xy, double l_z, int n_obs,
+                        const double* obs, int device, long long cap, int* ids, double* vals,
+                        double* min_out, long long* total_out);
+
 const char* st_last_error(void);
 int st_version(void);
 

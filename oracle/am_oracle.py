@@ -246,3 +246,38 @@ def min_normalized_distance(spec, traj) -> tuple[float, int]:
                     + ((traj[..., 2] - c[2]) / sz) ** 2)
         best, bad = min(best, float(v.min())), bad + int((v < 1).sum())
     return best, bad
+
+
+def check_collisions_scalar(traj, l_xy, l_z, obstacles=()):
+    """Scalar restatement of validation.py:39-93 (check_collisions), loop for loop.
+
+    Returns (minimum, violations) with violations as
+    ((kind, i, j_or_k), sample, value).  Pure Python: small cases only.
+    """
+    traj = np.asarray(traj, dtype=float)
+    n, m, _ = traj.shape
+    minimum = math.inf
+    viol = []
+    for i in range(n):
+        for j in range(i + 1, n):
+            for r in range(m):
+                dx = (float(traj[i, r, 0]) - float(traj[j, r, 0])) / l_xy
+                dy = (float(traj[i, r, 1]) - float(traj[j, r, 1])) / l_xy
+                dz = (float(traj[i, r, 2]) - float(traj[j, r, 2])) / l_z
+                v = math.sqrt(dx * dx + dy * dy + dz * dz)
+                minimum = min(minimum, v)
+                if v < 1.0:
+                    viol.append((("agent", i, j), r, v))
+    for i in range(n):
+        for k, (center, radius) in enumerate(obstacles):
+            sxy = l_xy / 2.0 + radius
+            sz = l_z / 2.0 + radius
+            for r in range(m):
+                dx = (float(traj[i, r, 0]) - center[0]) / sxy
+                dy = (float(traj[i, r, 1]) - center[1]) / sxy
+                dz = (float(traj[i, r, 2]) - center[2]) / sz
+                v = math.sqrt(dx * dx + dy * dy + dz * dz)
+                minimum = min(minimum, v)
+                if v < 1.0:
+                    viol.append((("obstacle", i, k), r, v))
+    return minimum, viol

@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "_swarm_am.so")
 # capi.cu holds the host side; the kernel variants are explicitly instantiated in inst_*.cu
 # so the (independent, slow) device compilations run in parallel
 SOURCES = [os.path.join(CSRC, f) for f in ("capi.cu", "inst_nb1_12.cu", "inst_nb1_16.cu", "inst_nb2.cu",
-                                           "inst_nb48.cu", "inst_experimental.cu")]
+                                           "inst_nb48.cu", "inst_experimental.cu", "collisions.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "am_kernel.cuh"), os.path.join(ROOT, "include", "swarm_am.h")]
 
 NVCC_FLAGS = [
@@ -48,13 +48,22 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
     if not force and not stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(CSRC, "obj")
+    import hashlib
+    tag = hashlib.sha1(" ".join(extra_flags).encode()).hexdigest()[:8] if extra_flags else ""
+    objdir = os.path.join(CSRC, "obj" + ("_" + tag if tag else ""))
     os.makedirs(objdir, exist_ok=True)
     log = os.path.join(HERE, "csrc", "build.log")
+
+    headers = [d for d in DEPS if d not in SOURCES]
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, *extra_flags, "-c", "-o", obj, src]
+        # incremental: an object newer than its source and every shared header is reused
+        # (A/B builds with extra flags keep their objects in their own directory)
+        if not force and os.path.exists(obj) and \
+                all(os.path.getmtime(obj) > os.path.getmtime(d) for d in [src, *headers]):
+            return cmd, obj, subprocess.CompletedProcess(cmd, 0, "", "(up to date)\n")
         return cmd, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:

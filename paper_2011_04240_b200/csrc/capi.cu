@@ -76,6 +76,9 @@ struct Launch {
 
 }  // namespace
 
+// shared with collisions.cu
+int swarm_fail(int code, const std::string& msg) { return fail(code, msg); }
+
 struct st_plan {
   int n, nobs, m, nv, S, device, nvmax;
   double* d_mats = nullptr;  // P | G | Gm | F | Fm | E | rho | packed stage mats | 1/rho

@@ -215,7 +215,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
         coeffs = out["c"][b]
         traj = np.ascontiguousarray(np.einsum("ank,tk->nta", coeffs, basis.P))
         tm0 = time.perf_counter()
-        rep_metrics = metrics.final_metrics(spec, traj) if with_metrics else {}
+        rep_metrics = metrics.final_metrics(spec, traj, device=config.device) if with_metrics else {}
         hist = out["hist"][b]
         timings = {
             "assembly_s": t1 - t0,

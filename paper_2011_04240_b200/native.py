@@ -23,7 +23,7 @@ _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedErro
 
 EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
            "st_last_error", "st_version", "st_shard_layout", "st_shard_buffer", "st_shard_open", "st_shard_close",
-           "st_shard_reset", "st_solve_sharded")
+           "st_shard_reset", "st_solve_sharded", "st_check_collisions")
 
 _lib = None
 _lock = threading.Lock()
@@ -59,6 +59,8 @@ def load() -> ctypes.CDLL:
         lib.st_shard_reset.argtypes = [vp, vp]
         lib.st_solve_sharded.argtypes = [vp, i, i, ctypes.POINTER(vp), _dp, _dp, _dp, i, i, d, _dp, _dp, _ip, _ip,
                                          ctypes.POINTER(ctypes.c_float)]
+        ll = ctypes.c_longlong
+        lib.st_check_collisions.argtypes = [i, i, _dp, d, d, i, _dp, i, ll, _ip, _dp, _dp, ctypes.POINTER(ll)]
         for name in EXPORTS:
             getattr(lib, name)  # every declared symbol must resolve
         _lib = lib
@@ -206,3 +208,31 @@ class Plan:
                                           t))
         return {"c": c_out, "hist": hist, "iters": iters, "converged": conv.astype(bool),
                 "timings_ms": tuple(float(x) for x in t)}
+
+
+def check_collisions(traj: np.ndarray, l_xy: float, l_z: float, obs_rows: np.ndarray, device: int = 0,
+                     cap: int = 4096):
+    """Device collision verdict (``st_check_collisions``; reference validation.py:39-93).
+
+    Returns (minimum, violations) with violations in the reference's order and
+    form: ``(("agent", i, j) | ("obstacle", i, k), sample, value)``.
+    """
+    lib = load()
+    traj = np.ascontiguousarray(traj, dtype=np.float64)
+    n, m = traj.shape[0], traj.shape[1]
+    obs_rows = np.ascontiguousarray(obs_rows, dtype=np.float64).reshape(-1, 5)
+    n_obs = obs_rows.shape[0]
+    mn, total = ctypes.c_double(), ctypes.c_longlong()
+    while True:
+        ids = np.empty((max(cap, 1), 4), dtype=np.int32)
+        vals = np.empty(max(cap, 1))
+        _check(lib.st_check_collisions(n, m, _ptr(traj), float(l_xy), float(l_z), n_obs,
+                                       _ptr(obs_rows) if n_obs else None, int(device), cap,
+                                       _ptr(ids, _ip), _ptr(vals), ctypes.byref(mn), ctypes.byref(total)))
+        if total.value <= cap:
+            break
+        cap = int(total.value)
+    kinds = ("agent", "obstacle")
+    viol = [((kinds[int(k)], int(i), int(j)), int(r), float(v))
+            for (k, i, j, r), v in zip(ids[: total.value].tolist(), vals[: total.value].tolist())]
+    return float(mn.value), viol

@@ -126,6 +126,9 @@ def _pair_worker(rank, world, port, out_q):
         return fake["p"]
 
     engine._plan_for = plan_for
+    # no GPU here: the post-solve collision check runs through the host restatement
+    from paper_2011_04240_b200 import metrics
+    metrics.check_collisions_device = lambda traj, geom, obs=(), device=0: metrics.check_collisions(traj, geom, obs)
     rep = am_solve_pair_sharded(spec, SolverConfig(max_iters=20, device=rank))
     out_q.put((rank, fake["p"].calls, None if rep is None else (rep.iterations, rep.converged,
                                                                  np.asarray(rep.coefficients).shape)))
