@@ -203,6 +203,71 @@ def _alpha_beta(diffs, l_xy, l_z):
     return alpha, beta
 
 
+def _pair_state(spec, coeffs, basis):
+    """Pair differences (solver.py:228-236), per-row semi-axes and projected angles of coefficients."""
+    n, n_obs, m = len(spec.start), len(spec.obstacles), basis.num_samples
+    X = np.einsum("ank,tk->ant", coeffs, basis.P)
+    ii, jj = np.triu_indices(n, k=1)
+    p = len(ii) + n * n_obs
+    diffs = np.empty((3, p, m))
+    diffs[:, : len(ii)] = X[:, ii] - X[:, jj]
+    lxy = np.full((p, 1), spec.geometry.l_xy)
+    lz = np.full((p, 1), spec.geometry.l_z)
+    for i in range(n):
+        for k, obs in enumerate(spec.obstacles):
+            row = len(ii) + i * n_obs + k
+            diffs[:, row] = X[:, i] - np.asarray(obs.center)[:, None]
+            lxy[row], lz[row] = obstacle_axes(spec, obs)
+    alpha, beta = _alpha_beta(diffs, lxy, lz)
+    return diffs, lxy, lz, alpha, beta
+
+
+def _augmented_cost(spec, basis, coeffs, alpha, beta, d, lam, rho) -> float:
+    """``augmented_cost`` (solver.py:285-303) of a state whose coefficients are ``coeffs``."""
+    diffs, lxy, lz, _, _ = _pair_state(spec, coeffs, basis)
+    sb = np.sin(beta)
+    target = (lxy * d * sb * np.cos(alpha), lxy * d * sb * np.sin(alpha), lz * d * np.cos(beta))
+    H = basis.Pddot.T @ basis.Pddot
+    total = 0.0
+    for axis in range(3):
+        c = coeffs[axis]
+        total += 0.5 * float(np.einsum("ik,kl,il->", c, H, c))
+        shifted = (diffs[axis] - target[axis]) + lam[axis] / rho
+        total += 0.5 * rho * float(np.sum(shifted * shifted))
+    return total
+
+
+def _descent_slack(spec, basis, plan, c0, beq, geom, schedule, config, iterations, final_coeffs) -> list:
+    """``descent_slack`` diagnostic (solver.py:413-421): augmented-cost change of every axis step.
+
+    The device loop solves the three axes together (they are independent given the
+    pair variables), so the diagnostic is rebuilt from prefix runs: the device state
+    after k iterations (``keep_state`` with ``max_iters=k`` and the full run's
+    ``switch_every``) is the reference's state entering iteration k, and the
+    coefficients after k+1 iterations are that iteration's axis solutions.  Untimed,
+    O(iterations^2) device iterations; the cost itself is evaluated on the host.
+    """
+    slack = []
+    states = {}
+    for k in range(1, iterations):
+        out = plan.solve(c0, beq, geom, schedule.switch_every, k, config.tolerance, keep_state=True,
+                         cluster_hint=config.cluster_size)
+        _, _, _, alpha, beta = _pair_state(spec, out["c"][0], basis)
+        states[k] = (out["c"][0], alpha, beta, out["d"], out["lam"])
+    for k in range(1, iterations):
+        c_k, alpha, beta, d, lam = states[k]
+        c_next = states[k + 1][0] if k + 1 < iterations else final_coeffs
+        rho = schedule.values[schedule.stage_for(k)]
+        mixed = c_k.copy()
+        before = _augmented_cost(spec, basis, mixed, alpha, beta, d, lam, rho)
+        for axis in range(3):
+            mixed[axis] = c_next[axis]
+            after = _augmented_cost(spec, basis, mixed, alpha, beta, d, lam, rho)
+            slack.append(after - before)
+            before = after
+    return slack
+
+
 def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with_metrics=True) -> list:
     """Device outputs of one launch -> one SolveReport per scenario (reference field layout)."""
     t0, t1, t2, t3 = stamps
@@ -231,19 +296,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
         }
         diagnostics = {}
         if config.keep_state:
-            p, m = plan.num_pairs, basis.num_samples
-            X = np.einsum("ank,tk->ant", coeffs, basis.P)
-            ii, jj = np.triu_indices(n, k=1)
-            diffs = np.empty((3, p, m))
-            diffs[:, : len(ii)] = X[:, ii] - X[:, jj]
-            lxy = np.full((p, 1), spec.geometry.l_xy)
-            lz = np.full((p, 1), spec.geometry.l_z)
-            for i in range(n):
-                for k, obs in enumerate(spec.obstacles):
-                    row = len(ii) + i * n_obs + k
-                    diffs[:, row] = X[:, i] - np.asarray(obs.center)[:, None]
-                    lxy[row], lz[row] = obstacle_axes(spec, obs)
-            alpha, beta = _alpha_beta(diffs, lxy, lz)
+            _, lxy, lz, alpha, beta = _pair_state(spec, coeffs, basis)
             lam = out["lam"]
             stage = schedule.stage_for(it - 1)
             diagnostics["final_state"] = FinalState(
@@ -277,9 +330,8 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
     specs = list(specs)
     if not specs:
         return []
-    if config.track_descent:
-        raise NotImplementedError("track_descent (an augmented-cost diagnostic between axis solves) is not "
-                                  "implemented by the device loop")
+    if config.track_descent and len(specs) != 1:
+        raise ValueError("track_descent is only available for single solves")
     for spec in specs:
         v = validate(spec)
         if v:
@@ -302,6 +354,9 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
                      keep_state=config.keep_state, cluster_hint=config.cluster_size)
     t3 = time.perf_counter()
     reports = _make_reports(specs, out, basis, plan, cache, schedule, config, (t0, t1, t2, t3), with_metrics)
+    if config.track_descent:
+        reports[0].diagnostics["descent_slack"] = _descent_slack(
+            spec0, basis, plan, c0, beq, geom, schedule, config, reports[0].iterations, reports[0].coefficients)
     log.info("batch of %d solved on device in %.3f ms", len(specs), out["timings_ms"][1])
     return reports
 

@@ -209,9 +209,10 @@ def test_batch_must_share_a_fingerprint():
         engine.am_solve_batch([generate_random(4, (8, 8, 3), 0.4, 0), generate_random(5, (8, 8, 3), 0.4, 0)])
 
 
-def test_track_descent_is_reported_unsupported():
-    with pytest.raises(NotImplementedError):
-        engine.am_solve(generate_random(4, (8, 8, 3), 0.4, 0), SolverConfig(track_descent=True))
+def test_track_descent_needs_a_single_solve():
+    specs = [generate_random(4, (8, 8, 3), 0.4, s) for s in (0, 1)]
+    with pytest.raises(ValueError, match="single"):
+        engine.am_solve_batch(specs, SolverConfig(track_descent=True))
 
 
 # --- collision metrics (reference validation.py) ------------------------------------------------------
