@@ -9,11 +9,11 @@
 // correctly rounded sqrt; no FMA contraction), so the minimum, the violation
 // count and every (pair, sample, value) entry are bit-identical.
 //
-// Three launches on one stream: (1) one warp per row: row minimum into a
-// global atomicMin (non-negative doubles order like their bit patterns) and
-// the row's violation count; (2) one block: exclusive scan of the counts;
-// (3) one warp per violating row: entries written at the row's offset in
-// sample order (ballot prefix).  HBM traffic is the trajectory (n*m*24 B,
+// Launches on one stream: (1) one warp per row: row minimum into a global
+// atomicMin (non-negative doubles order like their bit patterns), the row's
+// violation count, and the total; then, only when the total is non-zero,
+// (2) one block: exclusive scan of the counts; (3) one warp per violating
+// row: entries written at the row's offset in sample order (ballot prefix).  HBM traffic is the trajectory (n*m*24 B,
 // L2-resident) plus 8 B per row; the work is latency-bound and tiny next to
 // the solve, so the grid is simply rows/8 CTAs of 8 warps.
 #include <cuda_runtime.h>
@@ -107,7 +107,8 @@ __device__ __forceinline__ double row_value(const RowGeom& g, int r) {
 }
 
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) rows_kernel(Rows R, int* row_cnt,
-                                                                   unsigned long long* min_bits) {
+                                                                   unsigned long long* min_bits,
+                                                                   unsigned long long* count) {
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (row >= R.n_rows) return;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) rows_kernel(Rows R, int* 
   if (lane == 0) {
     row_cnt[row] = cnt;
     atomicMin(min_bits, (unsigned long long)__double_as_longlong(vmin));
+    if (cnt) atomicAdd(count, (unsigned long long)cnt);
   }
 }
 
@@ -248,20 +250,21 @@ extern "C" int st_check_collisions(int n, int m, const double* traj, double l_xy
   const unsigned long long inf_bits = 0x7ff0000000000000ULL;
   CC_CUDA(cudaMemcpyAsync(d_traj, traj, (size_t)n * m * 24, cudaMemcpyHostToDevice, s));
   if (n_obs) CC_CUDA(cudaMemcpyAsync(d_obs, obs, (size_t)n_obs * 40, cudaMemcpyHostToDevice, s));
-  CC_CUDA(cudaMemcpyAsync(d_min, &inf_bits, 8, cudaMemcpyHostToDevice, s));
+  const unsigned long long init[2] = {inf_bits, 0};
+  CC_CUDA(cudaMemcpyAsync(d_min, init, 16, cudaMemcpyHostToDevice, s));
   Rows R{d_traj, d_obs, n, m, n_obs, n_pairs, n_rows, l_xy, l_z};
   const unsigned grid = (unsigned)((n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  rows_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, d_cnt, d_min);
+  rows_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, d_cnt, d_min, (unsigned long long*)d_total);
   CC_CUDA(cudaGetLastError());
-  scan_kernel<<<1, 1024, 0, s>>>(d_cnt, d_off, n_rows, d_total);
-  CC_CUDA(cudaGetLastError());
-  unsigned long long min_bits = inf_bits;
-  long long total = 0;
-  CC_CUDA(cudaMemcpyAsync(&min_bits, d_min, 8, cudaMemcpyDeviceToHost, s));
-  CC_CUDA(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long res[2] = {inf_bits, 0};
+  CC_CUDA(cudaMemcpyAsync(res, d_min, 16, cudaMemcpyDeviceToHost, s));
   CC_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long min_bits = res[0];
+  const long long total = (long long)res[1];
   const long long take = total < cap ? total : cap;
-  if (take > 0) {
+  if (take > 0) {  // violations are rare on solved instances: scan + entries only when there are some
+    scan_kernel<<<1, 1024, 0, s>>>(d_cnt, d_off, n_rows, d_total);
+    CC_CUDA(cudaGetLastError());
     entries_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, d_cnt, d_off, cap, d_ids, d_vals);
     CC_CUDA(cudaGetLastError());
     CC_CUDA(cudaMemcpyAsync(ids, d_ids, (size_t)take * 16, cudaMemcpyDeviceToHost, s));
