@@ -17,8 +17,11 @@ follow reference ``pkg/src/swarmtraj/problem.py``:
 from __future__ import annotations
 
 import enum
+import functools
 import json
 import math
+
+import numpy as np
 import os
 from dataclasses import dataclass
 
@@ -147,15 +150,37 @@ def obstacle_axes(spec, obstacle) -> tuple[float, float]:
     return spec.geometry.l_xy / 2.0 + obstacle.radius, spec.geometry.l_z / 2.0 + obstacle.radius
 
 
+@functools.lru_cache(maxsize=16)
+def _pairs(n):
+    ii, jj = np.triu_indices(n, k=1)
+    ii.setflags(write=False)
+    jj.setflags(write=False)
+    return ii, jj
+
+
+def _near_pairs(P, l_xy, l_z):
+    """Vectorized prefilter: agent pairs (i<j, lexicographic) whose separation may be < 1."""
+    ii, jj = _pairs(P.shape[0])
+    d = (P[ii] - P[jj]) * np.array([1.0 / l_xy, 1.0 / l_xy, 1.0 / l_z])
+    keep = np.einsum("pk,pk->p", d, d) < (1.0 + 1e-9) ** 2
+    return zip(ii[keep].tolist(), jj[keep].tolist())
+
+
 def validate(spec) -> list[Violation]:
-    """Every start/goal separation violation (reference problem.py:162-194)."""
+    """Every start/goal separation violation (reference problem.py:162-194).
+
+    Same violations, order and text as the reference's O(n^2) scalar loop; a
+    vectorized prefilter picks the candidate pairs and the reference's scalar
+    expression decides each one, so the O(n^2) part costs no Python per pair.
+    """
     out: list[Violation] = []
     g = spec.geometry
     n = len(spec.start)
     for label, states in (("start", spec.start), ("goal", spec.goal)):
         pos = [s.position for s in states]
-        for i in range(n):
-            for j in range(i + 1, n):
+        if n > 1:
+            P = np.asarray(pos, dtype=float).reshape(n, 3)
+            for i, j in _near_pairs(P, g.l_xy, g.l_z):
                 sep = _separation(pos[i], pos[j], g.l_xy, g.l_z)
                 if sep < 1.0:
                     out.append(Violation(f"{label} pair ({i}, {j})", f"normalized separation {sep:.4f} < 1"))

@@ -244,3 +244,50 @@ def test_native_library_exports_every_declared_symbol():
     h = ctypes.c_void_p()
     assert lib.st_plan_create(0, 0, 10, 11, 1, None, None, None, None, None, None, None, 0, ctypes.byref(h)) == 1
     assert b"dimensions" in lib.st_last_error()
+
+
+def test_vectorized_validate_equals_scalar_loop():
+    """validate's prefilter must not change the reference's violations, order or text (problem.py:162-194)."""
+    import dataclasses
+
+    from paper_2011_04240_b200.spec import Violation, _separation, obstacle_axes, validate
+
+    def scalar(spec):
+        out, g, n = [], spec.geometry, len(spec.start)
+        for label, states in (("start", spec.start), ("goal", spec.goal)):
+            pos = [s.position for s in states]
+            for i in range(n):
+                for j in range(i + 1, n):
+                    sep = _separation(pos[i], pos[j], g.l_xy, g.l_z)
+                    if sep < 1.0:
+                        out.append(Violation(f"{label} pair ({i}, {j})", f"normalized separation {sep:.4f} < 1"))
+            for i in range(n):
+                for k, obs in enumerate(spec.obstacles):
+                    lxy, lz = obstacle_axes(spec, obs)
+                    sep = _separation(pos[i], obs.center, lxy, lz)
+                    if sep < 1.0:
+                        out.append(Violation(f"{label} agent {i} vs obstacle {k}",
+                                             f"normalized separation {sep:.4f} < 1"))
+        return out
+
+    rng = np.random.default_rng(0)
+    total = 0
+    for trial in range(25):
+        spec = generate_random(int(rng.integers(1, 25)), (8, 8, 3), 0.4, trial)
+        starts = tuple(dataclasses.replace(s, position=tuple((np.array(s.position) * rng.uniform(0.05, 1)).tolist()))
+                       for s in spec.start)
+        spec = dataclasses.replace(spec, start=starts)
+        got = validate(spec)
+        assert got == scalar(spec)
+        total += len(got)
+    assert total > 0
+
+
+def test_vectorized_trajectory_metrics_bitwise():
+    from paper_2011_04240_b200 import metrics
+    rng = np.random.default_rng(3)
+    for n, m in ((1, 3), (7, 10), (40, 100)):
+        traj = rng.normal(size=(n, m, 3)) * 3
+        q = metrics.trajectory_metrics(traj)
+        assert q.arc_length == tuple(metrics.arc_length(t) for t in traj)
+        assert q.smoothness == tuple(metrics.smoothness(t) for t in traj)
