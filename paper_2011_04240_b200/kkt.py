@@ -32,13 +32,25 @@ fingerprint, none inside the loop; kkt_cache.py:385-419).
 from __future__ import annotations
 
 import hashlib
+import json
+import logging
+import os
 import threading
+import time
+from pathlib import Path
 from dataclasses import dataclass, field
 
 import numpy as np
 from scipy.linalg import lu_factor
 
 from . import poly
+
+log = logging.getLogger(__name__)
+
+# on-disk entry files (kept apart from the reference's factors.npz / manifest.json, whose LU
+# factors are a different operator, so both caches can share one directory)
+OPERATORS_FILE = "b200_operators.npz"
+MANIFEST_FILE = "b200_manifest.json"
 
 BOUNDARY_ROWS = 6
 
@@ -158,7 +170,7 @@ class FactorCache:
         self._plans: dict = {}
         self._lock = threading.Lock()
         self._inflight: dict = {}
-        self.disk_dir = disk_dir
+        self.disk_dir = Path(disk_dir) if disk_dir else None
         self.factorizations = 0
         self.hits = 0
         self.misses = 0
@@ -186,11 +198,17 @@ class FactorCache:
                     break
             ev.wait()
         try:
-            op = stage_operator(basis, fp.num_agents, fp.num_obstacles, rho)
+            op = self._load_one(fp, rho)
+            built = op is None
+            if built:
+                op = stage_operator(basis, fp.num_agents, fp.num_obstacles, rho)
             with self._lock:
                 self._ops[key] = op
-                self.factorizations += 1
-                self.misses += 1
+                if built:
+                    self.factorizations += 1
+                    self.misses += 1
+                else:
+                    self.hits += 1
             return op
         finally:
             with self._lock:
@@ -198,6 +216,65 @@ class FactorCache:
 
     def prefactorize(self, fp: Fingerprint, basis: poly.Basis, schedule: RhoSchedule) -> list:
         return [self.get(fp, basis, rho) for rho in schedule.values]
+
+    # -- disk persistence (kkt_cache.py:458-528) ---------------------------------------------------
+    def _entry_dir(self, fp: Fingerprint):
+        return None if self.disk_dir is None else self.disk_dir / fp.key()
+
+    def _load_one(self, fp: Fingerprint, rho: float):
+        entry = self._entry_dir(fp)
+        if entry is None or not (entry / MANIFEST_FILE).exists():
+            return None
+        try:
+            manifest = json.loads((entry / MANIFEST_FILE).read_text())
+            if manifest["fingerprint"] != fp.key() or float(rho) not in manifest["rho_values"]:
+                return None
+            idx = manifest["rho_values"].index(float(rho))
+            with np.load(entry / OPERATORS_FILE) as blob:
+                parts = {name: blob[f"{name}_{idx}"] for name in ("G", "Gm", "F", "Fm")}
+        except (OSError, KeyError, ValueError) as exc:
+            log.warning("ignoring unreadable operator cache entry %s: %s", entry, exc)
+            return None
+        log.info("loaded cached stage operator %s rho=%g from %s", fp.key(), rho, entry)
+        return StageOperator(rho=float(rho), **parts)
+
+    def persist(self, fp: Fingerprint, basis: poly.Basis, schedule: RhoSchedule) -> dict:
+        """Build (or fetch) every stage and write them under ``disk_dir`` (kkt_cache.py:483-528).
+
+        Rewriting identical content is skipped (idempotent rebuilds); returns the manifest.
+        """
+        if self.disk_dir is None:
+            raise ValueError("cache has no disk directory configured")
+        t0 = time.perf_counter()
+        ops = self.prefactorize(fp, basis, schedule)
+        entry = self._entry_dir(fp)
+        entry.mkdir(parents=True, exist_ok=True)
+        manifest = {
+            "fingerprint": fp.key(),
+            "num_agents": fp.num_agents,
+            "num_samples": fp.num_samples,
+            "num_coeffs": fp.num_coeffs,
+            "num_obstacles": fp.num_obstacles,
+            "basis_kind": fp.basis_kind,
+            "basis_sha": fp.basis_sha,
+            "rho_values": [op.rho for op in ops],
+            "operator": "structured 17x17 stage blocks (G, Gm, F, Fm)",
+            "block_dimension": fp.num_coeffs + BOUNDARY_ROWS,
+        }
+        path = entry / MANIFEST_FILE
+        text = json.dumps(manifest, indent=2) + "\n"
+        if not (path.exists() and path.read_text() == text and (entry / OPERATORS_FILE).exists()):
+            blobs = {f"{name}_{i}": getattr(op, name) for i, op in enumerate(ops) for name in ("G", "Gm", "F", "Fm")}
+            tmp = entry / (OPERATORS_FILE + ".tmp")
+            with open(tmp, "wb") as fh:
+                np.savez(fh, **blobs)
+            os.replace(tmp, entry / OPERATORS_FILE)
+            tmp_manifest = entry / (MANIFEST_FILE + ".tmp")
+            tmp_manifest.write_text(text)
+            os.replace(tmp_manifest, path)
+        manifest["build_time_s"] = time.perf_counter() - t0
+        manifest["bytes"] = (entry / OPERATORS_FILE).stat().st_size
+        return manifest
 
     def plan(self, fp: Fingerprint, schedule: RhoSchedule, build):
         """Device plan for (fingerprint, rho values), created once via ``build()``."""

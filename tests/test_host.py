@@ -291,3 +291,33 @@ def test_vectorized_trajectory_metrics_bitwise():
         q = metrics.trajectory_metrics(traj)
         assert q.arc_length == tuple(metrics.arc_length(t) for t in traj)
         assert q.smoothness == tuple(metrics.smoothness(t) for t in traj)
+
+
+def test_disk_cache_roundtrip(tmp_path):
+    """Mirrors the reference's test_kkt.py:292-316 for the structured stage operators."""
+    from paper_2011_04240_b200 import kkt, poly
+    spec = generate_random(2, (8, 8, 3), 0.4, 0)
+    basis = poly.for_spec(spec)
+    fp = kkt.fingerprint(basis, 2, 0)
+    schedule = kkt.build_rho_schedule(1.0, 2.0, 3, 30)
+    writer = kkt.FactorCache(disk_dir=tmp_path)
+    manifest = writer.persist(fp, basis, schedule)
+    assert manifest["rho_values"] == [1.0, 2.0, 4.0]
+    entry = tmp_path / manifest["fingerprint"]
+    assert (entry / kkt.OPERATORS_FILE).exists()
+    before = (entry / kkt.MANIFEST_FILE).read_bytes()
+    kkt.FactorCache(disk_dir=tmp_path).persist(fp, basis, schedule)
+    assert (entry / kkt.MANIFEST_FILE).read_bytes() == before  # idempotent rebuild
+    reader = kkt.FactorCache(disk_dir=tmp_path)
+    op = reader.get(fp, basis, 2.0)
+    assert reader.stats()["factorizations"] == 0 and reader.stats()["hits"] == 1  # loaded, not rebuilt
+    fresh = kkt.stage_operator(basis, 2, 0, 2.0)
+    for name in ("G", "Gm", "F", "Fm"):
+        np.testing.assert_array_equal(getattr(op, name), getattr(fresh, name))
+    # a rho outside the manifest is built, and a corrupt entry is ignored with a rebuild
+    reader.get(fp, basis, 8.0)
+    assert reader.stats()["factorizations"] == 1
+    (entry / kkt.OPERATORS_FILE).write_bytes(b"not an npz")
+    broken = kkt.FactorCache(disk_dir=tmp_path)
+    broken.get(fp, basis, 1.0)
+    assert broken.stats()["factorizations"] == 1
