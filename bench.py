@@ -17,8 +17,13 @@ whole batch (every scenario to convergence or max_iters) in one device launch.
   (profiles/ubench_r1.txt: 64 lanes/clk/SM x 148 SMs x SM clock x 2).
 * ``cpu_baseline``: the reference algorithm (oracle/am_oracle.py, numpy/scipy LU path,
   warm factors) on a bounded sample, one process per host core.
-* Multi-GPU (torchrun): scenarios are sharded over ranks (strong scaling, no
-  data-path collective; NCCL only for the barrier and the max-over-ranks timing).
+* Multi-GPU (torchrun): scenarios are independent units, so ranks shard them with no
+  data-path collective (NCCL only for the barrier and the max-over-ranks timing).
+  Default ``--scaling weak``: every rank solves its own batch of ``--batch`` scenarios
+  (rank r: seeds r*batch .. (r+1)*batch-1), value = all scenarios / max-over-ranks time.
+  ``--scaling strong``: the one batch of ``--batch`` (seeds 0..batch-1) split 1/N per rank
+  (BASELINE config 4 read literally; at N=8 each GPU gets 128 scenarios for 74 clusters,
+  so two cluster rounds bound it at ~6.6x).
 
 ``--impl reference`` times the reference algorithm on the host cores instead.
 """
@@ -169,7 +174,7 @@ def run_reference(args):
     sample = f"{per_core * cores} rand32 scenarios (seeds 1024..) per step, warm LU factors, 1 process/core"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": 1e3 * vals[-1]["wall_s"],
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "rand32 batch (generate_random(32,(8,8,3),0.4,seed))",
                                             "agents": 32, "samples": 100, "degree": 10},
             "cpu_baseline": {"value": v, "unit": "solves/s", "cores": cores, "kind": "port", "sample": sample},
@@ -201,6 +206,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--cpu-per-core", type=int, default=2, help="cpu_baseline sample: scenarios per core")
     ap.add_argument("--ref-per-core", type=int, default=1)
     ap.add_argument("--warmup-ref", type=int, default=0)
@@ -219,7 +225,12 @@ def main():
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    lo, hi = rank * args.batch // world, (rank + 1) * args.batch // world
+    if args.scaling == "weak":
+        lo, hi = rank * args.batch, (rank + 1) * args.batch
+        total = args.batch * world
+    else:
+        lo, hi = rank * args.batch // world, (rank + 1) * args.batch // world
+        total = args.batch
     specs = scenarios(lo, hi)
     B = len(specs)
     cfg = SolverConfig(device=local)
@@ -270,7 +281,7 @@ def main():
     barrier(world)
     dev_ms_max = allreduce_max(dev_ms, world, dev)
     step_ms = dev_ms_max / args.steps
-    value = args.batch / (step_ms / 1e3)
+    value = total / (step_ms / 1e3)
 
     # end to end through the C ABI with page-locked host buffers (H2D of the inputs + loop +
     # D2H of the results inside the timed region, every step)
@@ -323,15 +334,18 @@ def main():
     ach_bytes = BYTES_PER_PAIR_SAMPLE * pair_samples / (dev_ms / args.steps / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "solves/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"batch of {args.batch} rand32 scenarios (generate_random(32,(8,8,3),0.4,seed), "
-                               f"seeds 0..{args.batch - 1}), 1/N per rank", "agents": 32, "samples": m,
+        "config": {"workload": (f"batch of {args.batch} rand32 scenarios per GPU (generate_random(32,(8,8,3),0.4,"
+                                f"seed), rank r: seeds r*{args.batch}..(r+1)*{args.batch}-1)"
+                                if args.scaling == "weak" else
+                                f"batch of {args.batch} rand32 scenarios (generate_random(32,(8,8,3),0.4,seed), "
+                                f"seeds 0..{args.batch - 1}), 1/N per rank"), "agents": 32, "samples": m,
                    "degree": 10, "max_iters": cfg.max_iters, "tol": cfg.tolerance,
                    "cluster_ctas": launch_cfg["cluster"], "clusters": launch_cfg["clusters"],
                    "lambda_in_smem": bool(launch_cfg["lambda_in_smem"]),
                    "l2": "flushed (256 MB write) between timed steps"},
-        "e2e": {"value": round(args.batch / e2e_s, 2), "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+        "e2e": {"value": round(total / e2e_s, 2), "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "path": "C ABI st_solve, page-locked host buffers"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(fp64_peak_tflops, 2),
