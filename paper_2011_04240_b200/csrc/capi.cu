@@ -253,8 +253,20 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       T.fn = ke->fn;
       T.c_global = cg_try;
       T.stream = lam == swarm::LAM_STREAM ? 1 : 0;
-      const long long base = layout(pl, T, C);
-      const long long need = base + (pass == 0 ? T.lam_per_cta : 0);
+      long long base = layout(pl, T, C);
+      long long need = base + (pass == 0 ? T.lam_per_cta : 0);
+      const char* mc0 = std::getenv("SWARM_MULTI_CLUSTER");
+      const bool want_multi = G > 1 || (batch == 1 && C > 1 && (mc0 ? std::atoi(mc0) != 0 : pl->n > 32));
+      if (need > bud && want_multi) {
+        // one cluster cannot hold the scenario's per-CTA buffers, but K co-resident clusters
+        // (each CTA owning ~m/(G K C) samples) may: size the layout for the multi-cluster split
+        int nsm = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
+        T.G = G;
+        T.K = std::max(1, std::min(std::max(1, nsm / C), pl->m / (G * C)));
+        base = layout(pl, T, C);
+        need = base + (pass == 0 ? T.lam_per_cta : 0);
+      }
       if (need > bud) continue;
       T.lam_smem = pass == 0 ? 1 : 0;
       T.lam_tail = 0;
@@ -287,6 +299,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
         cudaGetLastError();
         continue;
       }
+      if (T.K > 1 && !(active > 1 && want_multi)) continue;  // sized for a split that cannot run
       T.nclusters = std::min(batch, active);
       // one large scenario: spread it over every co-resident cluster (grid barrier per iteration)
       const char* mc = std::getenv("SWARM_MULTI_CLUSTER");
@@ -416,6 +429,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
         av.accessPolicyWindow.num_bytes = std::min(used, (size_t)max_window);
         av.accessPolicyWindow.hitRatio =
             (float)std::min(1.0, (double)max_persist / std::max(1.0, gfrac * av.accessPolicyWindow.num_bytes));
+        if (const char* hr = std::getenv("SWARM_L2_HIT")) av.accessPolicyWindow.hitRatio = (float)std::atof(hr);
         av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);

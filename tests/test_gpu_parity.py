@@ -78,6 +78,18 @@ def test_cluster_size_does_not_change_results_beyond_rounding(cuda_ok, cluster):
     assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref)
 
 
+@pytest.mark.parametrize("cluster", [10, 5, 4])
+def test_large_scenario_multi_cluster_splits_match_reference(cuda_ok, cluster):
+    """n = 256 over K clusters of C CTAs (K*C = 100 or 80: one sample per CTA, or 1-2), sized
+    for the split even though a single cluster of C cannot hold the scenario."""
+    from paper_2011_04240_b200 import am_solve
+    spec, cfg, ref = load_golden("rand256_s0")
+    rep = am_solve(spec, _config(cfg, cluster_size=cluster))
+    assert rep.iterations == int(ref["iterations"])
+    assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref)
+    assert rep.metrics["num_collision_violations"] == int(ref["num_collision_violations"])
+
+
 def test_batch_equals_single_solves_bitwise(cuda_ok):
     from paper_2011_04240_b200 import am_solve, am_solve_batch, generate_random
     specs = [generate_random(16, (8, 8, 3), 0.4, s) for s in range(12)]
