@@ -99,7 +99,21 @@ class Fingerprint:
         return hashlib.sha256(text.encode()).hexdigest()[:16]
 
 
+_DIGESTS: dict = {}
+
+
 def basis_digest(basis: poly.Basis) -> str:
+    hit = _DIGESTS.get(id(basis))
+    if hit is not None and hit[0] is basis:
+        return hit[1]
+    d = _basis_digest(basis)
+    if len(_DIGESTS) > 64:
+        _DIGESTS.clear()
+    _DIGESTS[id(basis)] = (basis, d)  # keeps the basis alive, so the id cannot be reused
+    return d
+
+
+def _basis_digest(basis: poly.Basis) -> str:
     h = hashlib.sha256()
     for a in (basis.P, basis.Pdot, basis.Pddot):
         h.update(np.ascontiguousarray(a).tobytes())

@@ -12,6 +12,7 @@ Pddot are bitwise identical to ``swarmtraj.build_basis`` output.
 
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import dataclass, field
 
@@ -83,8 +84,14 @@ def build(num_samples: int, duration: float, degree: int, kind=BasisKind.BERNSTE
         raise ValueError(f"duration must be positive, got {duration}")
     if degree < MIN_DEGREE:
         raise ValueError(f"degree must be >= {MIN_DEGREE}, got {degree}")
-    kind = BasisKind(kind)
+    return _build(int(num_samples), float(duration), int(degree), BasisKind(kind))
+
+
+@functools.lru_cache(maxsize=64)
+def _build(num_samples: int, duration: float, degree: int, kind: BasisKind) -> Basis:
+    # one immutable Basis per (m, duration, degree, kind): every solve of a fingerprint reuses it
     samples = np.linspace(0.0, float(duration), num_samples)
+    samples.setflags(write=False)
     tau = samples / float(duration)
     fam = _bernstein_family if kind == BasisKind.BERNSTEIN else _monomial_family
     b, d1, d2 = fam(tau, degree)
