@@ -119,6 +119,13 @@ int st_check_collisions(int n, int m, const double* traj, double l_xy, double l_
                         const double* obs, int device, long long cap, int* ids, double* vals,
                         double* min_out, long long* total_out);
 
+/* The same verdict for B scenarios of one shape in one pass: traj B x n x m x 3,
+ * geom B x 2 (l_xy, l_z), obs B x n_obs x 5; min_out[B], total_out[B]; entries
+ * scenario-major (scenario b's after those of scenarios < b), min(sum, cap) written. */
+int st_check_collisions_batch(int B, int n, int m, const double* traj, const double* geom, int n_obs,
+                              const double* obs, int device, long long cap, int* ids, double* vals,
+                              double* min_out, long long* total_out);
+
 const char* st_last_error(void);
 int st_version(void);
 

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/swarm_am.h"
 
@@ -33,11 +34,11 @@ namespace {
 constexpr int kWarpsPerBlock = 8;
 
 struct Rows {
-  const double* traj;  // n x m x 3
-  const double* obs;   // n_obs x 5: cx, cy, cz, sep_xy, sep_z
+  const double* traj;  // B x n x m x 3
+  const double* obs;   // B x n_obs x 5: cx, cy, cz, sep_xy, sep_z
+  const double* geom;  // B x 2: l_xy, l_z
   int n, m, n_obs;
   long long n_pairs, n_rows;
-  double l_xy, l_z;
 };
 
 // (i, j) of agent pair `row` in (i<j) lexicographic order
@@ -59,24 +60,25 @@ struct RowGeom {
   int kind, i, k;
 };
 
-__device__ __forceinline__ RowGeom row_geom(const Rows& R, long long row) {
+__device__ __forceinline__ RowGeom row_geom(const Rows& R, int scn, long long row) {
   RowGeom g;
+  const double* traj = R.traj + (size_t)scn * R.n * R.m * 3;
   if (row < R.n_pairs) {
     int i, j;
     pair_of(row, R.n, i, j);
-    g.a = R.traj + (size_t)i * R.m * 3;
-    g.b = R.traj + (size_t)j * R.m * 3;
+    g.a = traj + (size_t)i * R.m * 3;
+    g.b = traj + (size_t)j * R.m * 3;
     g.c0 = g.c1 = g.c2 = 0.0;
-    g.sxy = R.l_xy;
-    g.sz = R.l_z;
+    g.sxy = R.geom[2 * scn];
+    g.sz = R.geom[2 * scn + 1];
     g.kind = 0;
     g.i = i;
     g.k = j;
   } else {
     long long o = row - R.n_pairs;
     int i = (int)(o / R.n_obs), k = (int)(o % R.n_obs);
-    const double* ob = R.obs + (size_t)k * 5;
-    g.a = R.traj + (size_t)i * R.m * 3;
+    const double* ob = R.obs + ((size_t)scn * R.n_obs + k) * 5;
+    g.a = traj + (size_t)i * R.m * 3;
     g.b = nullptr;
     g.c0 = ob[0];
     g.c1 = ob[1];
@@ -111,8 +113,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) rows_kernel(Rows R, int* 
                                                                    unsigned long long* count) {
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int scn = blockIdx.y;
   if (row >= R.n_rows) return;
-  const RowGeom g = row_geom(R, row);
+  const RowGeom g = row_geom(R, scn, row);
   double vmin = INFINITY;
   int cnt = 0;
   for (int r0 = 0; r0 < R.m; r0 += 32) {
@@ -123,19 +126,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) rows_kernel(Rows R, int* 
   }
   for (int s = 16; s; s >>= 1) vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, s));
   if (lane == 0) {
-    row_cnt[row] = cnt;
-    atomicMin(min_bits, (unsigned long long)__double_as_longlong(vmin));
-    if (cnt) atomicAdd(count, (unsigned long long)cnt);
+    row_cnt[(size_t)scn * R.n_rows + row] = cnt;
+    atomicMin(min_bits + scn, (unsigned long long)__double_as_longlong(vmin));
+    if (cnt) atomicAdd(count + scn, (unsigned long long)cnt);
   }
 }
 
-// exclusive scan of row counts (one block of 1024 threads, chunked); total into *total
-__global__ void __launch_bounds__(1024) scan_kernel(const int* row_cnt, long long* row_off, long long n_rows,
-                                                    long long* total) {
+// exclusive scan of one scenario's row counts (one block of 1024 threads per scenario, chunked),
+// offset by the scenario's first entry base[scenario]
+__global__ void __launch_bounds__(1024) scan_kernel(const int* row_cnt_all, long long* row_off_all, long long n_rows,
+                                                    const long long* base) {
+  const int* row_cnt = row_cnt_all + (size_t)blockIdx.x * n_rows;
+  long long* row_off = row_off_all + (size_t)blockIdx.x * n_rows;
   __shared__ long long warp_sums[32];
   __shared__ long long carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = base[blockIdx.x];
   __syncthreads();
   for (long long base = 0; base < n_rows; base += 1024) {
     const long long idx = base + threadIdx.x;
@@ -161,7 +167,6 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int* row_cnt, long lon
     if (threadIdx.x == 1023) carry = c + warp_sums[warp] + x;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
 }
 
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) entries_kernel(Rows R, const int* row_cnt,
@@ -169,9 +174,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) entries_kernel(Rows R, co
                                                                       int* ids, double* vals) {
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (row >= R.n_rows || row_cnt[row] == 0) return;
-  const RowGeom g = row_geom(R, row);
-  long long pos = row_off[row];
+  const int scn = blockIdx.y;
+  if (row >= R.n_rows || row_cnt[(size_t)scn * R.n_rows + row] == 0) return;
+  const RowGeom g = row_geom(R, scn, row);
+  long long pos = row_off[(size_t)scn * R.n_rows + row];
   for (int r0 = 0; r0 < R.m; r0 += 32) {
     const int r = r0 + lane;
     const double v = r < R.m ? row_value(g, r) : INFINITY;
@@ -211,25 +217,30 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
-extern "C" int st_check_collisions(int n, int m, const double* traj, double l_xy, double l_z, int n_obs,
-                                   const double* obs, int device, long long cap, int* ids, double* vals,
-                                   double* min_out, long long* total_out) {
-  if (n < 0 || m < 0 || n_obs < 0 || cap < 0) return swarm_fail(ST_EINVAL, "negative size");
+extern "C" int st_check_collisions_batch(int B, int n, int m, const double* traj, const double* geom, int n_obs,
+                                         const double* obs, int device, long long cap, int* ids, double* vals,
+                                         double* min_out, long long* total_out) {
+  if (B < 0 || n < 0 || m < 0 || n_obs < 0 || cap < 0) return swarm_fail(ST_EINVAL, "negative size");
+  if (B > 65535) return swarm_fail(ST_EINVAL, "batch larger than 65535 scenarios");
   if (device < 0 || device >= 64) return swarm_fail(ST_EINVAL, "bad device ordinal");
-  if (!min_out || !total_out || (n * m > 0 && !traj) || (n_obs > 0 && !obs) || (cap > 0 && (!ids || !vals)))
+  if (B > 0 && (!min_out || !total_out || !geom || (n * m > 0 && !traj) || (n_obs > 0 && !obs)))
     return swarm_fail(ST_EINVAL, "NULL buffer");
+  if (cap > 0 && (!ids || !vals)) return swarm_fail(ST_EINVAL, "NULL buffer");
   const long long n_pairs = (long long)n * (n - 1) / 2, n_rows = n_pairs + (long long)n * n_obs;
-  *min_out = INFINITY;
-  *total_out = 0;
-  if (n_rows == 0 || m == 0) return ST_OK;
+  for (int b = 0; b < B; ++b) {
+    min_out[b] = INFINITY;
+    total_out[b] = 0;
+  }
+  if (B == 0 || n_rows == 0 || m == 0) return ST_OK;
   Scratch& S = g_scratch[device];
   std::lock_guard<std::mutex> guard(S.mu);
   CC_CUDA(cudaSetDevice(device));
   if (!S.stream) CC_CUDA(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
-  const size_t b_traj = align256((size_t)n * m * 24), b_obs = align256((size_t)n_obs * 40 + 8),
-               b_cnt = align256((size_t)n_rows * 4), b_off = align256((size_t)n_rows * 8), b_misc = 256,
+  const size_t b_traj = align256((size_t)B * n * m * 24), b_obs = align256((size_t)B * n_obs * 40 + 8),
+               b_geom = align256((size_t)B * 16), b_cnt = align256((size_t)B * n_rows * 4),
+               b_off = align256((size_t)B * n_rows * 8), b_misc = align256((size_t)B * 24),
                b_ids = align256((size_t)cap * 16), b_vals = align256((size_t)cap * 8);
-  const size_t need = b_traj + b_obs + b_cnt + b_off + b_misc + b_ids + b_vals;
+  const size_t need = b_traj + b_obs + b_geom + b_cnt + b_off + b_misc + b_ids + b_vals;
   if (need > S.bytes) {
     if (S.buf) cudaFree(S.buf);
     S.buf = nullptr;
@@ -240,30 +251,46 @@ extern "C" int st_check_collisions(int n, int m, const double* traj, double l_xy
   char* p = (char*)S.buf;
   double* d_traj = (double*)p;
   double* d_obs = (double*)(p += b_traj);
-  int* d_cnt = (int*)(p += b_obs);
+  double* d_geom = (double*)(p += b_obs);
+  int* d_cnt = (int*)(p += b_geom);
   long long* d_off = (long long*)(p += b_cnt);
-  unsigned long long* d_min = (unsigned long long*)(p += b_off);
-  long long* d_total = (long long*)(d_min + 1);
+  unsigned long long* d_min = (unsigned long long*)(p += b_off);  // B minima | B totals | B bases
+  unsigned long long* d_total = d_min + B;
+  long long* d_base = (long long*)(d_total + B);
   int* d_ids = (int*)(p += b_misc);
   double* d_vals = (double*)(p += b_ids);
   cudaStream_t s = S.stream;
   const unsigned long long inf_bits = 0x7ff0000000000000ULL;
-  CC_CUDA(cudaMemcpyAsync(d_traj, traj, (size_t)n * m * 24, cudaMemcpyHostToDevice, s));
-  if (n_obs) CC_CUDA(cudaMemcpyAsync(d_obs, obs, (size_t)n_obs * 40, cudaMemcpyHostToDevice, s));
-  const unsigned long long init[2] = {inf_bits, 0};
-  CC_CUDA(cudaMemcpyAsync(d_min, init, 16, cudaMemcpyHostToDevice, s));
-  Rows R{d_traj, d_obs, n, m, n_obs, n_pairs, n_rows, l_xy, l_z};
-  const unsigned grid = (unsigned)((n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  rows_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, d_cnt, d_min, (unsigned long long*)d_total);
+  std::vector<unsigned long long> res(2 * (size_t)B);
+  for (int b = 0; b < B; ++b) {
+    res[b] = inf_bits;
+    res[B + b] = 0;
+  }
+  CC_CUDA(cudaMemcpyAsync(d_traj, traj, (size_t)B * n * m * 24, cudaMemcpyHostToDevice, s));
+  if (n_obs) CC_CUDA(cudaMemcpyAsync(d_obs, obs, (size_t)B * n_obs * 40, cudaMemcpyHostToDevice, s));
+  CC_CUDA(cudaMemcpyAsync(d_geom, geom, (size_t)B * 16, cudaMemcpyHostToDevice, s));
+  CC_CUDA(cudaMemcpyAsync(d_min, res.data(), 16 * (size_t)B, cudaMemcpyHostToDevice, s));
+  Rows R{d_traj, d_obs, d_geom, n, m, n_obs, n_pairs, n_rows};
+  const dim3 grid((unsigned)((n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock), (unsigned)B);
+  rows_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, d_cnt, d_min, d_total);
   CC_CUDA(cudaGetLastError());
-  unsigned long long res[2] = {inf_bits, 0};
-  CC_CUDA(cudaMemcpyAsync(res, d_min, 16, cudaMemcpyDeviceToHost, s));
+  CC_CUDA(cudaMemcpyAsync(res.data(), d_min, 16 * (size_t)B, cudaMemcpyDeviceToHost, s));
   CC_CUDA(cudaStreamSynchronize(s));
-  const unsigned long long min_bits = res[0];
-  const long long total = (long long)res[1];
-  const long long take = total < cap ? total : cap;
+  // scenario-major entry list: scenario b starts after the entries of scenarios < b
+  std::vector<long long> base(B);
+  long long all = 0;
+  for (int b = 0; b < B; ++b) {
+    base[b] = all;
+    all += (long long)res[B + b];
+    double mn;
+    memcpy(&mn, &res[b], 8);
+    min_out[b] = mn;
+    total_out[b] = (long long)res[B + b];
+  }
+  const long long take = all < cap ? all : cap;
   if (take > 0) {  // violations are rare on solved instances: scan + entries only when there are some
-    scan_kernel<<<1, 1024, 0, s>>>(d_cnt, d_off, n_rows, d_total);
+    CC_CUDA(cudaMemcpyAsync(d_base, base.data(), 8 * (size_t)B, cudaMemcpyHostToDevice, s));
+    scan_kernel<<<B, 1024, 0, s>>>(d_cnt, d_off, n_rows, d_base);
     CC_CUDA(cudaGetLastError());
     entries_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, d_cnt, d_off, cap, d_ids, d_vals);
     CC_CUDA(cudaGetLastError());
@@ -271,9 +298,13 @@ extern "C" int st_check_collisions(int n, int m, const double* traj, double l_xy
     CC_CUDA(cudaMemcpyAsync(vals, d_vals, (size_t)take * 8, cudaMemcpyDeviceToHost, s));
     CC_CUDA(cudaStreamSynchronize(s));
   }
-  double mn;
-  memcpy(&mn, &min_bits, 8);
-  *min_out = mn;
-  *total_out = total;
   return ST_OK;
+}
+
+extern "C" int st_check_collisions(int n, int m, const double* traj, double l_xy, double l_z, int n_obs,
+                                   const double* obs, int device, long long cap, int* ids, double* vals,
+                                   double* min_out, long long* total_out) {
+  if (!min_out || !total_out) return swarm_fail(ST_EINVAL, "NULL buffer");
+  const double geom[2] = {l_xy, l_z};
+  return st_check_collisions_batch(1, n, m, traj, geom, n_obs, obs, device, cap, ids, vals, min_out, total_out);
 }

@@ -274,13 +274,21 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
     h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
     n, n_obs = len(specs[0].start), len(specs[0].obstacles)
     reports = []
+    # per scenario (a batched einsum may sum in another order): batch and single solves report
+    # bitwise-identical trajectories and metrics
+    trajs = np.stack([np.einsum("ank,tk->nta", c, basis.P) for c in out["c"]])
+    tc0 = time.perf_counter()
+    cols = (metrics.check_collisions_device_batch(trajs, specs, config.device) if with_metrics and len(specs) > 1
+            else [None] * len(specs))
+    col_s = (time.perf_counter() - tc0) / len(specs)
     for b, spec in enumerate(specs):
         it = int(out["iters"][b])
         cache.count_solve(3 * it)
         coeffs = out["c"][b]
-        traj = np.ascontiguousarray(np.einsum("ank,tk->nta", coeffs, basis.P))
+        traj = trajs[b]
         tm0 = time.perf_counter()
-        rep_metrics = metrics.final_metrics(spec, traj, device=config.device) if with_metrics else {}
+        rep_metrics = (metrics.final_metrics(spec, traj, device=config.device, collisions=cols[b])
+                       if with_metrics else {})
         hist = out["hist"][b]
         timings = {
             "assembly_s": t1 - t0,
@@ -290,7 +298,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
             "h2d_s": h2d_ms / 1e3,
             "d2h_s": d2h_ms / 1e3,
             "solve_call_s": t3 - t2,
-            "metrics_s": time.perf_counter() - tm0,
+            "metrics_s": time.perf_counter() - tm0 + (col_s if cols[b] is not None else 0.0),
             "total_s": time.perf_counter() - t0,
             "batch": len(specs),
         }

@@ -23,7 +23,8 @@ _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedErro
 
 EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
            "st_last_error", "st_version", "st_shard_layout", "st_shard_buffer", "st_shard_open", "st_shard_close",
-           "st_shard_reset", "st_solve_sharded", "st_check_collisions")
+           "st_shard_reset", "st_solve_sharded", "st_check_collisions",
+           "st_check_collisions_batch")
 
 _lib = None
 _lock = threading.Lock()
@@ -61,6 +62,8 @@ def load() -> ctypes.CDLL:
                                          ctypes.POINTER(ctypes.c_float)]
         ll = ctypes.c_longlong
         lib.st_check_collisions.argtypes = [i, i, _dp, d, d, i, _dp, i, ll, _ip, _dp, _dp, ctypes.POINTER(ll)]
+        lib.st_check_collisions_batch.argtypes = [i, i, i, _dp, _dp, i, _dp, i, ll, _ip, _dp, _dp,
+                                                  ctypes.POINTER(ll)]
         for name in EXPORTS:
             getattr(lib, name)  # every declared symbol must resolve
         _lib = lib
@@ -236,3 +239,35 @@ def check_collisions(traj: np.ndarray, l_xy: float, l_z: float, obs_rows: np.nda
     viol = [((kinds[int(k)], int(i), int(j)), int(r), float(v))
             for (k, i, j, r), v in zip(ids[: total.value].tolist(), vals[: total.value].tolist())]
     return float(mn.value), viol
+
+
+def check_collisions_batch(trajs: np.ndarray, geoms: np.ndarray, obs_rows: np.ndarray, device: int = 0,
+                           cap: int = 4096) -> list:
+    """``st_check_collisions_batch``: one (minimum, violations) per scenario, one device pass."""
+    lib = load()
+    trajs = np.ascontiguousarray(trajs, dtype=np.float64)
+    B, n, m = trajs.shape[0], trajs.shape[1], trajs.shape[2]
+    geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(B, 2)
+    obs_rows = np.ascontiguousarray(obs_rows, dtype=np.float64).reshape(B, -1, 5)
+    n_obs = obs_rows.shape[1]
+    mins = np.empty(B)
+    totals = np.empty(B, dtype=np.int64)
+    tp = ctypes.POINTER(ctypes.c_longlong)
+    while True:
+        ids = np.empty((max(cap, 1), 4), dtype=np.int32)
+        vals = np.empty(max(cap, 1))
+        _check(lib.st_check_collisions_batch(B, n, m, _ptr(trajs), _ptr(geoms), n_obs,
+                                             _ptr(obs_rows) if n_obs else None, int(device), cap, _ptr(ids, _ip),
+                                             _ptr(vals), _ptr(mins), _ptr(totals, tp)))
+        if int(totals.sum()) <= cap:
+            break
+        cap = int(totals.sum())
+    kinds = ("agent", "obstacle")
+    out, e = [], 0
+    ids_l, vals_l = ids.tolist(), vals.tolist()
+    for b in range(B):
+        t = int(totals[b])
+        out.append((float(mins[b]), [((kinds[k], i, j), r, v) for (k, i, j, r), v in
+                                     zip(ids_l[e:e + t], vals_l[e:e + t])]))
+        e += t
+    return out

@@ -81,3 +81,34 @@ def test_device_check_collisions_equals_host_on_solutions(cuda_ok, name):
     assert dev.min_normalized_distance == host.min_normalized_distance
     assert dev.violations == host.violations
     assert len(dev.violations) == int(ref["num_collision_violations"])
+
+
+@pytest.mark.gpu
+def test_device_batch_equals_per_scenario(cuda_ok):
+    from paper_2011_04240_b200 import metrics
+    from paper_2011_04240_b200.spec import AgentGeometry, Obstacle
+    rng = np.random.default_rng(11)
+    B, n, m, n_obs = 6, 9, 37, 2
+    trajs = rng.uniform(-0.5, 0.5, (B, n, m, 3))
+    specs = []
+    for b in range(B):
+        geom = AgentGeometry(0.8, 0.6 + 0.1 * b)
+        obstacles = tuple(Obstacle(tuple(rng.uniform(-2, 2, 3).tolist()), float(rng.uniform(0.1, 0.5)))
+                          for _ in range(n_obs))
+        specs.append(type("S", (), {"geometry": geom, "obstacles": obstacles})())
+    got = metrics.check_collisions_device_batch(trajs, specs)
+    assert sum(len(g.violations) for g in got) > 4096  # the entry list outgrows the first capacity
+    for b in range(B):
+        mn, viol = _oracle(trajs[b], specs[b].geometry, specs[b].obstacles)
+        assert got[b].min_normalized_distance == mn
+        assert got[b].violations == viol
+
+
+@pytest.mark.gpu
+def test_batch_reports_carry_the_per_scenario_verdicts(cuda_ok):
+    from paper_2011_04240_b200 import am_solve_batch, generate_random, metrics
+    specs = [generate_random(8, (8, 8, 3), 0.4, s) for s in range(5)]
+    reps = am_solve_batch(specs)
+    for spec, rep in zip(specs, reps):
+        # one batched device verdict per launch == the host restatement on the same trajectories
+        assert rep.metrics == metrics.final_metrics(spec, rep.trajectories)
