@@ -274,9 +274,10 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
     h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
     n, n_obs = len(specs[0].start), len(specs[0].obstacles)
     reports = []
-    # per scenario (a batched einsum may sum in another order): batch and single solves report
-    # bitwise-identical trajectories and metrics
-    trajs = np.stack([np.einsum("ank,tk->nta", c, basis.P) for c in out["c"]])
+    # trajectories exactly as the reference forms them (solver.py:133-136: c_axis @ P.T per axis),
+    # per scenario, so batch and single solves report identical trajectories and metrics
+    PT = basis.P.T
+    trajs = np.stack([np.stack([c[a] @ PT for a in range(3)], axis=-1) for c in out["c"]])
     tc0 = time.perf_counter()
     cols = (metrics.check_collisions_device_batch(trajs, specs, config.device) if with_metrics and len(specs) > 1
             else [None] * len(specs))
