@@ -135,17 +135,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) rows_kernel(Rows R, int* 
 // exclusive scan of one scenario's row counts (one block of 1024 threads per scenario, chunked),
 // offset by the scenario's first entry base[scenario]
 __global__ void __launch_bounds__(1024) scan_kernel(const int* row_cnt_all, long long* row_off_all, long long n_rows,
-                                                    const long long* base) {
+                                                    const long long* first) {
+  constexpr int kPer = 4;  // consecutive rows per thread: 4096 rows per block pass
   const int* row_cnt = row_cnt_all + (size_t)blockIdx.x * n_rows;
   long long* row_off = row_off_all + (size_t)blockIdx.x * n_rows;
   __shared__ long long warp_sums[32];
   __shared__ long long carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = base[blockIdx.x];
+  if (threadIdx.x == 0) carry = first[blockIdx.x];
   __syncthreads();
-  for (long long base = 0; base < n_rows; base += 1024) {
-    const long long idx = base + threadIdx.x;
-    long long v = idx < n_rows ? row_cnt[idx] : 0, x = v;
+  for (long long chunk = 0; chunk < n_rows; chunk += 1024 * kPer) {
+    const long long idx0 = chunk + (long long)threadIdx.x * kPer;
+    long long v[kPer], own = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      v[e] = idx0 + e < n_rows ? row_cnt[idx0 + e] : 0;
+      own += v[e];
+    }
+    long long x = own;  // inclusive scan of per-thread sums
     for (int s = 1; s < 32; s <<= 1) {
       long long y = __shfl_up_sync(0xffffffffu, x, s);
       if (lane >= s) x += y;
@@ -162,9 +169,14 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int* row_cnt_all, long
     }
     __syncthreads();
     const long long c = carry;
-    if (idx < n_rows) row_off[idx] = c + warp_sums[warp] + x - v;
+    long long run = c + warp_sums[warp] + x - own;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      if (idx0 + e < n_rows) row_off[idx0 + e] = run;
+      run += v[e];
+    }
     __syncthreads();
-    if (threadIdx.x == 1023) carry = c + warp_sums[warp] + x;
+    if (threadIdx.x == 1023) carry = run;
     __syncthreads();
   }
 }
