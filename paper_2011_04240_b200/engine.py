@@ -279,7 +279,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
     PT = basis.P.T
     trajs = np.stack([np.stack([c[a] @ PT for a in range(3)], axis=-1) for c in out["c"]])
     tc0 = time.perf_counter()
-    cols = (metrics.check_collisions_device_batch(trajs, specs, config.device) if with_metrics and len(specs) > 1
+    cols = (metrics.collision_summary_device_batch(trajs, specs, config.device) if with_metrics
             else [None] * len(specs))
     col_s = (time.perf_counter() - tc0) / len(specs)
     for b, spec in enumerate(specs):

@@ -242,8 +242,14 @@ def check_collisions(traj: np.ndarray, l_xy: float, l_z: float, obs_rows: np.nda
 
 
 def check_collisions_batch(trajs: np.ndarray, geoms: np.ndarray, obs_rows: np.ndarray, device: int = 0,
-                           cap: int = 4096) -> list:
-    """``st_check_collisions_batch``: one (minimum, violations) per scenario, one device pass."""
+                           cap: int = 4096, count_only: bool = False) -> list:
+    """``st_check_collisions_batch``: one (minimum, violations) per scenario, one device pass.
+
+    ``count_only``: (minimum, number of violations) per scenario -- what the report's metrics
+    need -- from the row pass alone (no entry list is built or copied).
+    """
+    if count_only:
+        cap = 0
     lib = load()
     trajs = np.ascontiguousarray(trajs, dtype=np.float64)
     B, n, m = trajs.shape[0], trajs.shape[1], trajs.shape[2]
@@ -259,9 +265,11 @@ def check_collisions_batch(trajs: np.ndarray, geoms: np.ndarray, obs_rows: np.nd
         _check(lib.st_check_collisions_batch(B, n, m, _ptr(trajs), _ptr(geoms), n_obs,
                                              _ptr(obs_rows) if n_obs else None, int(device), cap, _ptr(ids, _ip),
                                              _ptr(vals), _ptr(mins), _ptr(totals, tp)))
-        if int(totals.sum()) <= cap:
+        if count_only or int(totals.sum()) <= cap:
             break
         cap = int(totals.sum())
+    if count_only:
+        return [(float(mn), int(t)) for mn, t in zip(mins.tolist(), totals.tolist())]
     kinds = ("agent", "obstacle")
     out, e = [], 0
     ids_l, vals_l = ids.tolist(), vals.tolist()

@@ -128,7 +128,11 @@ def _pair_worker(rank, world, port, out_q):
     engine._plan_for = plan_for
     # no GPU here: the post-solve collision check runs through the host restatement
     from paper_2011_04240_b200 import metrics
-    metrics.check_collisions_device = lambda traj, geom, obs=(), device=0: metrics.check_collisions(traj, geom, obs)
+    def host_summary(trajs, specs, device=0):
+        cols = [metrics.check_collisions(t, sp.geometry, sp.obstacles) for t, sp in zip(trajs, specs)]
+        return [(c.min_normalized_distance, len(c.violations)) for c in cols]
+
+    metrics.collision_summary_device_batch = host_summary
     rep = am_solve_pair_sharded(spec, SolverConfig(max_iters=20, device=rank))
     out_q.put((rank, fake["p"].calls, None if rep is None else (rep.iterations, rep.converged,
                                                                  np.asarray(rep.coefficients).shape)))
