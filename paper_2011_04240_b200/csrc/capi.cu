@@ -212,6 +212,20 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
   std::vector<int> cands;
   if (hint > 0) {
     cands.push_back(hint);
+  } else if (batch == 1 && pl->n > 32) {
+    // latency, one large scenario over K clusters of C CTAs (multi-cluster): fewest samples per
+    // CTA first (the grid barrier waits for the fullest CTA), then the widest cluster. m = 100
+    // on 148 SMs: C = 10 (K = 10, one sample per CTA) -- measured 18 ms vs 34 ms for C = 16
+    // (K = 6, up to two samples per CTA) on rand256_s0
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
+    nsm = std::max(nsm, 1);
+    cands = {16, 10, 8, 5, 4, 2, 1};
+    auto per_cta = [&](int C) {
+      const int K = std::max(1, std::min(nsm / C, pl->m / C));
+      return ceil_div(pl->m, K * C);
+    };
+    std::stable_sort(cands.begin(), cands.end(), [&](int a, int b) { return per_cta(a) < per_cta(b); });
   } else if (batch == 1) {
     cands = {16, 8, 4, 2, 1};  // latency: spread one scenario widest
   } else {
