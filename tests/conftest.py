@@ -22,9 +22,10 @@ def pytest_configure(config):
 
 
 def golden_names():
-    # full-solve fixtures; descent_*.npz hold only descent_slack vectors (tests/test_descent.py)
+    # full-solve fixtures; descent_*.npz hold only descent_slack vectors (tests/test_descent.py),
+    # batch_*.npz per-seed vectors of the batched path (tests/test_batch_parity.py)
     names = (os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
-    return sorted(n for n in names if not n.startswith("descent_"))
+    return sorted(n for n in names if not n.startswith(("descent_", "batch_")))
 
 
 def load_golden(name):
