@@ -23,8 +23,10 @@
  * (agent, obstacle) agent-major (kkt_cache.py:197-215).
  * Return value: 0 ok; ST_EINVAL bad argument; ST_ECUDA CUDA failure;
  * ST_ENOMEM device allocation failure; ST_EUNSUPPORTED shape outside the
- * compiled kernels.  Plans are safe to share between threads (calls on one
- * plan serialize).
+ * compiled kernels.  Plans are safe to share between threads: host calls on one
+ * plan serialize on its mutex, and every launch on a plan is ordered after the
+ * previous one on the device (an event), whatever stream the caller passes, so
+ * solves sharing the plan's workspaces never overlap.
  */
 #ifndef SWARM_AM_H
 #define SWARM_AM_H
@@ -40,6 +42,15 @@ extern "C" {
 #define ST_EUNSUPPORTED 4
 
 #define ST_FLAG_KEEP_STATE 1 /* write final multipliers/d (batch must be 1) */
+#define ST_FLAG_FP32 2       /* FP32 pair state: multipliers and pair arithmetic in FP32,
+                                positions, right-hand-side sums and the KKT solve in FP64
+                                (north star's optional FP32 mode; tolerances in DESIGN.md §8) */
+
+/* Per-scenario status written to converged[]: */
+#define ST_CONVERGED 1
+#define ST_NOT_CONVERGED 0
+#define ST_NONFINITE (-1) /* the pair state became NaN/inf: where the reference's
+                             _check_ranges assertion fires (solver.py:355-360) */
 
 typedef struct st_plan st_plan;
 
@@ -63,7 +74,8 @@ int st_plan_destroy(st_plan* plan);
  *   cluster_hint: CTAs per scenario (0 = choose)
  * Outputs: c_out (batch x 3 x n x nv), hist (batch x 3 x max_iters:
  * residual norm, residual max-abs, boundary max per iteration), iters,
- * converged (batch).  lam_out (3 x p x m) and d_out (p x m) only with
+ * converged (batch: ST_CONVERGED / ST_NOT_CONVERGED / ST_NONFINITE).
+ * lam_out (3 x p x m) and d_out (p x m) only with
  * ST_FLAG_KEEP_STATE, else may be NULL.  timings_ms (may be NULL):
  * [h2d, device loop, d2h]. */
 int st_solve(st_plan* plan, int batch, const double* c0, const double* b_eq, const double* geom,
@@ -99,10 +111,10 @@ int st_solve_sharded(st_plan* plan, int G, int rank, void* const* bufs, const do
                      const double* geom, int switch_every, int max_iters, double tol, double* c_out,
                      double* hist, int* iters, int* converged, float* timings_ms);
 
-/* Launch configuration st_solve would use: out[0..7] = cluster size C,
- * agent blocks NB, lane segment width W, threads per CTA, lambda-in-smem flag,
- * dynamic smem bytes, clusters launched, steps per warp task. */
-int st_query_launch(st_plan* plan, int batch, int cluster_hint, long long* out8);
+/* Launch configuration st_solve would use (flags as for st_solve): out[0..7] =
+ * cluster size C, agent blocks NB, lane segment width W, threads per CTA,
+ * lambda-in-smem flag, dynamic smem bytes, clusters launched, steps per warp task. */
+int st_query_launch(st_plan* plan, int batch, int cluster_hint, int flags, long long* out8);
 
 /* Post-solve safety verdict (replaces validation.py:39-93, check_collisions,
  * called by _final_metrics, solver.py:497-509).  Host buffers.

@@ -6,7 +6,7 @@ out.  The AM loop itself runs in hand-written sm_100a CUDA behind the C ABI
 in ``include/swarm_am.h``.
 """
 
-from .engine import (FinalState, InfeasibleProblemError, Multipliers, PairVariables, SolveReport,
+from .engine import (FinalState, InfeasibleProblemError, NonFiniteStateError, Multipliers, PairVariables, SolveReport,
                      SolverConfig, am_solve, am_solve_batch, default_cache, pack)
 from .kkt import (FactorCache, Fingerprint, RhoSchedule, StageOperator, build_rho_schedule, fingerprint,
                   stage_operator)

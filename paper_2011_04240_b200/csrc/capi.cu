@@ -36,38 +36,34 @@ using KernelFn = void (*)(swarm::KParams);
 
 struct KernelEntry {
   int NB, NT, NVMAX, LAM;
+  bool f32;  // FP32 pair state (multipliers and pair arithmetic in FP32, FP64 solve)
   KernelFn fn;
-  int minb = 1;  // CTAs per SM the kernel is register-bounded for
 };
 
 using swarm::am_cluster_kernel;
-constexpr int kS = swarm::LAM_SMEM, kG = swarm::LAM_GLOBAL, kK = swarm::LAM_GLOBAL_KEEP, kT = swarm::LAM_STREAM;
+constexpr int kS = swarm::LAM_SMEM, kG = swarm::LAM_GLOBAL, kK = swarm::LAM_GLOBAL_KEEP;
+#define ST_K(NB, NT, NV, L, F) {NB, NT, NV, L, F, am_cluster_kernel<NB, NT, NV, L, F>}
 // lambda fits in shared memory only for n <= 32 (NB == 1); larger fleets stream it from L2.
 const KernelEntry kKernels[] = {
-    {1, 512, 12, kS, am_cluster_kernel<1, 512, 12, kS>}, {1, 512, 12, kG, am_cluster_kernel<1, 512, 12, kG>},
-    {1, 512, 12, kK, am_cluster_kernel<1, 512, 12, kK>}, {1, 512, 16, kS, am_cluster_kernel<1, 512, 16, kS>},
-    {1, 512, 16, kG, am_cluster_kernel<1, 512, 16, kG>}, {1, 512, 16, kK, am_cluster_kernel<1, 512, 16, kK>},
-    {2, 384, 12, kG, am_cluster_kernel<2, 384, 12, kG>}, {2, 384, 12, kK, am_cluster_kernel<2, 384, 12, kK>},
-    {2, 384, 16, kG, am_cluster_kernel<2, 384, 16, kG>}, {2, 384, 16, kK, am_cluster_kernel<2, 384, 16, kK>},
-    {4, 256, 12, kG, am_cluster_kernel<4, 256, 12, kG>}, {4, 256, 12, kK, am_cluster_kernel<4, 256, 12, kK>},
-    {8, 256, 12, kG, am_cluster_kernel<8, 256, 12, kG>}, {8, 256, 12, kK, am_cluster_kernel<8, 256, 12, kK>},
-#ifdef SWARM_EXPERIMENTAL_KERNELS
-    // measured slower than the defaults, built only with -DSWARM_EXPERIMENTAL_KERNELS:
-    // multipliers streamed through shared memory by TMA bulk copies (LAM_STREAM, SWARM_LAM_STREAM=1)
-    {1, 512, 12, kT, am_cluster_kernel<1, 512, 12, kT>}, {1, 512, 16, kT, am_cluster_kernel<1, 512, 16, kT>},
-    {2, 384, 12, kT, am_cluster_kernel<2, 384, 12, kT>}, {2, 384, 16, kT, am_cluster_kernel<2, 384, 16, kT>},
-    {4, 256, 12, kT, am_cluster_kernel<4, 256, 12, kT>}, {8, 256, 12, kT, am_cluster_kernel<8, 256, 12, kT>},
-    // two CTAs per SM (SWARM_DUAL=1)
-    {1, 256, 12, kG, am_cluster_kernel<1, 256, 12, kG, 2>, 2}, {1, 256, 16, kG, am_cluster_kernel<1, 256, 16, kG, 2>, 2},
-#endif
+    ST_K(1, 512, 12, kS, false), ST_K(1, 512, 12, kG, false), ST_K(1, 512, 12, kK, false),
+    ST_K(1, 512, 16, kS, false), ST_K(1, 512, 16, kG, false), ST_K(1, 512, 16, kK, false),
+    ST_K(2, 384, 12, kG, false), ST_K(2, 384, 12, kK, false), ST_K(2, 384, 16, kG, false),
+    ST_K(2, 384, 16, kK, false), ST_K(4, 256, 12, kG, false), ST_K(4, 256, 12, kK, false),
+    ST_K(8, 256, 12, kG, false), ST_K(8, 256, 12, kK, false),
+    ST_K(1, 512, 12, kS, true),  ST_K(1, 512, 12, kG, true),  ST_K(1, 512, 12, kK, true),
+    ST_K(1, 512, 16, kS, true),  ST_K(1, 512, 16, kG, true),  ST_K(1, 512, 16, kK, true),
+    ST_K(2, 384, 12, kG, true),  ST_K(2, 384, 12, kK, true),  ST_K(2, 384, 16, kG, true),
+    ST_K(2, 384, 16, kK, true),  ST_K(4, 256, 12, kG, true),  ST_K(4, 256, 12, kK, true),
+    ST_K(8, 256, 12, kG, true),  ST_K(8, 256, 12, kK, true),
 };
+#undef ST_K
 
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
   int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_tail = 0;
   int G = 1;  // groups (GPUs) sharing the scenario; participants = G x K clusters
-  int stream = 0;  // LAM_STREAM: per-warp TMA rings for the multipliers
+  int f32 = 0;    // FP32 pair state: multipliers are 4-byte elements
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -96,6 +92,8 @@ struct st_plan {
   size_t io_bytes = 0;
   int smem_optin = 0;
   int smem_sm = 0;  // shared memory per SM
+  int persist_set = 0;
+  cudaEvent_t ev_done = nullptr;  // last launch that used this plan's workspaces
   std::mutex mu;
 };
 
@@ -169,37 +167,40 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_bb, 18);
   take(k.o_wp, 2LL * NW);
   take(k.o_misc, 2);
-  take(k.o_ring, L.stream ? (long long)NW * swarm::LS_R * swarm::LS_K * 96 : 0);
-  take(k.o_mbar, L.stream ? (long long)NW * (swarm::LS_R + 1) : 0);
   k.o_lam = (int)o;
   L.lam_per_cta = (long long)L.tasks_max * L.nsteps * 96;
   return o;
 }
+
+// shared-memory doubles taken by `rows` multiplier rows (96 elements each)
+long long lam_rows_dbl(const Launch& L, long long rows) { return (rows * 96 * (L.f32 ? 4 : 8) + 7) / 8; }
 
 // Hybrid multipliers: rows per warp kept in shared memory (each warp's last rows), from
 // `spare` doubles of shared memory, at most the rows of the longest warp range.
 int tail_rows(const Launch& L, long long spare) {
   const int NW = L.NT / 32, TPW = 32 / L.W;
   const long long rows_max = ceil_div((long long)ceil_div(L.tmax, TPW) * L.nsteps, NW);
-  return (int)std::max(0LL, std::min(rows_max, spare / (96LL * NW)));
+  const long long per_row = 96LL * NW * (L.f32 ? 4 : 8) / 8;  // doubles per row across the warps
+  return (int)std::max(0LL, std::min(rows_max, spare / per_row));
 }
 
-const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, int minb = 1) {
+const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, bool f32) {
   for (const auto& e : kKernels)
-    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM && e.minb == minb) return &e;
+    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM && e.f32 == f32) return &e;
   return nullptr;
 }
 
-int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G = 1) {
+int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G = 1, bool f32 = false) {
   const int n = pl->n;
   if (n < 1 || n > 256) return fail(ST_EUNSUPPORTED, "n_agents must be in [1, 256] for the compiled kernels");
   const int nb_need = n <= 32 ? 1 : ceil_div(n, 32);
   int NB = 0;
   for (int cand : {1, 2, 4, 8})
-    if (cand >= nb_need && find_kernel(cand, pl->nvmax, swarm::LAM_GLOBAL)) { NB = cand; break; }
+    if (cand >= nb_need && find_kernel(cand, pl->nvmax, swarm::LAM_GLOBAL, f32)) { NB = cand; break; }
   if (!NB) return fail(ST_EUNSUPPORTED, "no compiled kernel for this agent count and basis degree");
   L.NB = NB;
   L.NVMAX = pl->nvmax;
+  L.f32 = f32 ? 1 : 0;
   if (NB == 1) {
     int w = 2;
     while (w < n) w <<= 1;
@@ -209,6 +210,9 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
   }
   L.nsteps = std::max(1, count_steps(n, pl->nobs, NB));  // n = 1, no obstacles: one empty step
   const long long budget = pl->smem_optin / 8;
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
+  nsm = std::max(nsm, 1);
   std::vector<int> cands;
   if (hint > 0) {
     cands.push_back(hint);
@@ -217,9 +221,6 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     // CTA first (the grid barrier waits for the fullest CTA), then the widest cluster. m = 100
     // on 148 SMs: C = 10 (K = 10, one sample per CTA) -- measured 18 ms vs 34 ms for C = 16
     // (K = 6, up to two samples per CTA) on rand256_s0
-    int nsm = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
-    nsm = std::max(nsm, 1);
     cands = {16, 10, 8, 5, 4, 2, 1};
     auto per_cta = [&](int C) {
       const int K = std::max(1, std::min(nsm / C, pl->m / C));
@@ -244,103 +245,106 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     for (int pass = 0; pass < 2; ++pass)
       for (int C : cands) order.push_back({C, pass});
   }
+  const char* mc_env = std::getenv("SWARM_MULTI_CLUSTER");
   for (int cg_try = 0; cg_try < 2; ++cg_try)
   for (const auto& cp : order) {
     const int C = cp.first, pass = cp.second;
     if (cg_try == 1 && pass == 0) continue;  // coefficients in global memory only with lambda there too
-    const char* lst = std::getenv("SWARM_LAM_STREAM");
-    const bool stream = (lst ? std::atoi(lst) != 0 : false) && find_kernel(NB, pl->nvmax, swarm::LAM_STREAM);
-    const int lam = pass == 0 ? swarm::LAM_SMEM
-                              : (keep ? swarm::LAM_GLOBAL_KEEP : (stream ? swarm::LAM_STREAM : swarm::LAM_GLOBAL));
+    const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
     if (keep && pass == 0) continue;
-    // batches with lambda in L2: two CTAs (two scenarios) per SM when the dual kernel exists
-    const char* du = std::getenv("SWARM_DUAL");
-    const bool dual = throughput && pass == 1 && !keep && (du ? std::atoi(du) != 0 : false);
-    const KernelEntry* ke = dual ? find_kernel(NB, pl->nvmax, lam, 2) : nullptr;
-    if (!ke) ke = find_kernel(NB, pl->nvmax, lam);
+    const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam, f32);
     if (!ke) continue;
-    const long long bud = ke->minb == 2 ? (pl->smem_sm / 2 - 1024) / 8 : budget;
-    {
-      if ((long long)C * G > pl->m || C < 1 || C > 16) continue;  // every CTA owns >= 1 sample
-      Launch T = L;
-      T.NT = ke->NT;
-      T.fn = ke->fn;
-      T.c_global = cg_try;
-      T.stream = lam == swarm::LAM_STREAM ? 1 : 0;
-      long long base = layout(pl, T, C);
-      long long need = base + (pass == 0 ? T.lam_per_cta : 0);
-      const char* mc0 = std::getenv("SWARM_MULTI_CLUSTER");
-      const bool want_multi = G > 1 || (batch == 1 && C > 1 && (mc0 ? std::atoi(mc0) != 0 : pl->n > 32));
-      if (need > bud && want_multi) {
-        // one cluster cannot hold the scenario's per-CTA buffers, but K co-resident clusters
-        // (each CTA owning ~m/(G K C) samples) may: size the layout for the multi-cluster split
-        int nsm = 0;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device);
-        T.G = G;
-        T.K = std::max(1, std::min(std::max(1, nsm / C), pl->m / (G * C)));
-        base = layout(pl, T, C);
-        need = base + (pass == 0 ? T.lam_per_cta : 0);
-      }
-      if (need > bud) continue;
-      T.lam_smem = pass == 0 ? 1 : 0;
-      T.lam_tail = 0;
-      long long need2 = need;
-      if (pass == 1 && !keep && !T.stream) {
-        // hybrid: spare shared memory holds the first groups of lambda (the rest stays in L2)
-        const char* hy = std::getenv("SWARM_LAM_HYBRID");
-        if (!hy || std::atoi(hy) != 0) {
-          T.lam_tail = tail_rows(T, bud - need);
-          need2 = need + (long long)T.lam_tail * 96 * (T.NT / 32);
-        }
-      }
-      T.smem_bytes = (size_t)need2 * 8;
-      ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_bytes));
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(C);
-      cfg.blockDim = dim3(T.NT);
-      cfg.dynamicSmemBytes = T.smem_bytes;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = C;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int active = 0;
-      cudaError_t e = cudaOccupancyMaxActiveClusters(&active, (void*)T.fn, &cfg);
-      if (e != cudaSuccess || active < 1) {
-        cudaGetLastError();
-        continue;
-      }
-      if (T.K > 1 && !(active > 1 && want_multi)) continue;  // sized for a split that cannot run
-      T.nclusters = std::min(batch, active);
-      // one large scenario: spread it over every co-resident cluster (grid barrier per iteration)
-      const char* mc = std::getenv("SWARM_MULTI_CLUSTER");
-      const bool multi = G > 1 || (batch == 1 && C > 1 && active > 1 && (mc ? std::atoi(mc) != 0 : pl->n > 32));
-      if (multi) {
-        Launch M = T;
-        M.G = G;
-        M.K = std::min(active, std::max(1, pl->m / (G * C)));
-        const long long mbase = layout(pl, M, C);
-        long long mneed = mbase + (pass == 0 ? M.lam_per_cta : 0);
-        M.lam_tail = 0;
-        if (pass == 1 && !keep && !M.stream && mneed <= budget) {
-          M.lam_tail = tail_rows(M, budget - mneed);
-          mneed += (long long)M.lam_tail * 96 * (M.NT / 32);
-        }
-        if (mneed <= budget) {
-          M.smem_bytes = (size_t)mneed * 8;
-          ST_CUDA(cudaFuncSetAttribute(M.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M.smem_bytes));
-          M.nclusters = M.K;
-          T = M;
-        }
-      }
-      L = T;
-      return 0;
+    if ((long long)C * G > pl->m || C < 1 || C > 16) continue;  // every CTA owns >= 1 sample
+    Launch T = L;
+    T.NT = ke->NT;
+    T.fn = ke->fn;
+    T.c_global = cg_try;
+    long long base = layout(pl, T, C);
+    long long need = base + (pass == 0 ? lam_rows_dbl(T, (long long)T.tasks_max * T.nsteps) : 0);
+    const bool want_multi = G > 1 || (batch == 1 && C > 1 && (mc_env ? std::atoi(mc_env) != 0 : pl->n > 32));
+    bool sized_for_split = false;
+    if (need > budget && want_multi) {
+      // one cluster cannot hold the scenario's per-CTA buffers, but K co-resident clusters
+      // (each CTA owning ~m/(G K C) samples) may: size the layout for the multi-cluster split
+      T.G = G;
+      T.K = std::max(1, std::min(std::max(1, nsm / C), pl->m / (G * C)));
+      base = layout(pl, T, C);
+      need = base + (pass == 0 ? lam_rows_dbl(T, (long long)T.tasks_max * T.nsteps) : 0);
+      sized_for_split = T.K > 1;
     }
+    if (need > budget) continue;
+    T.lam_smem = pass == 0 ? 1 : 0;
+    T.lam_tail = 0;
+    long long need2 = need;
+    if (pass == 1 && !keep) {
+      // hybrid: spare shared memory holds each warp's last multiplier rows (the rest stays in L2)
+      const char* hy = std::getenv("SWARM_LAM_HYBRID");
+      if (!hy || std::atoi(hy) != 0) {
+        T.lam_tail = tail_rows(T, budget - need);
+        need2 = need + lam_rows_dbl(T, (long long)T.lam_tail * (T.NT / 32));
+      }
+    }
+    T.smem_bytes = (size_t)need2 * 8;
+    ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_bytes));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(T.NT);
+    cfg.dynamicSmemBytes = T.smem_bytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int active = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&active, (void*)T.fn, &cfg);
+    if (e != cudaSuccess || active < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    // one large scenario: spread it over co-resident clusters (grid barrier per iteration)
+    const bool multi = G > 1 || (batch == 1 && C > 1 && active > 1 && want_multi);
+    if (sized_for_split && !multi) continue;  // sized for a split that cannot run
+    T.nclusters = std::min(batch, active);
+    if (multi) {
+      Launch M = T;
+      M.G = G;
+      M.K = std::min(active, std::max(1, pl->m / (G * C)));
+      const long long mbase = layout(pl, M, C);
+      long long mneed = mbase + (pass == 0 ? lam_rows_dbl(M, (long long)M.tasks_max * M.nsteps) : 0);
+      M.lam_tail = 0;
+      if (pass == 1 && !keep && mneed <= budget) {
+        M.lam_tail = tail_rows(M, budget - mneed);
+        mneed += lam_rows_dbl(M, (long long)M.lam_tail * (M.NT / 32));
+      }
+      if (mneed <= budget) {
+        M.smem_bytes = (size_t)mneed * 8;
+        ST_CUDA(cudaFuncSetAttribute(M.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M.smem_bytes));
+        M.nclusters = M.K;
+        T = M;
+      } else if (T.K > 1) {
+        continue;  // the split layout does not fit: never launch K > 1 on fewer clusters (advice r1)
+      }
+    }
+    if (T.K > 1 && T.nclusters != T.K) continue;  // a grid barrier needs all K clusters launched
+    L = T;
+    return 0;
   }
   return fail(ST_EUNSUPPORTED, "no cluster configuration fits this problem on the device");
+}
+
+// device-wide ordering of grid-barrier (multi-cluster) launches, one event per device
+std::mutex g_multi_mu;
+cudaEvent_t multi_event(int device) {
+  static cudaEvent_t evs[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!evs[device] && cudaEventCreateWithFlags(&evs[device], cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return evs[device];
 }
 
 struct ShardExt {
@@ -353,6 +357,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
         int* conv, double* lam_out, double* d_out, cudaStream_t s, const ShardExt* ext = nullptr) {
   Launch L = L0;
   swarm::KParams& k = L.kp;
+  ST_CUDA(cudaStreamWaitEvent(s, pl->ev_done, 0));  // previous launch on this plan has finished
   k.n = pl->n; k.nobs = pl->nobs; k.m = pl->m; k.nv = pl->nv; k.S = pl->S;
   k.P = pl->P; k.G = pl->G; k.Gm = pl->Gm; k.F = pl->F; k.Fm = pl->Fm; k.E = pl->E; k.rho = pl->rho;
   k.mats = pl->mats; k.inv_rho = pl->inv_rho;
@@ -415,8 +420,9 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
     }
     k.c_ws = pl->d_cws;
   }
+  const size_t esize = L.f32 ? sizeof(float) : sizeof(double);
   if (!L.lam_smem) {
-    const size_t need = (size_t)L.nclusters * L.C * L.lam_per_cta * sizeof(double);
+    const size_t need = (size_t)L.nclusters * L.C * L.lam_per_cta * esize;
     if (need > pl->lam_bytes) {
       if (pl->d_lam) cudaFree(pl->d_lam);
       pl->d_lam = nullptr;
@@ -425,34 +431,6 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       pl->lam_bytes = need;
     }
     k.lam_ws = pl->d_lam;
-    // keep the lambda slabs resident in L2 (persisting window) unless disabled
-    const char* pe = std::getenv("SWARM_L2_PERSIST");
-    if (!pe || std::atoi(pe) != 0) {
-      int dev = 0, max_persist = 0, max_window = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-      const size_t used = (size_t)L.nclusters * L.C * L.lam_per_cta * sizeof(double);
-      const int TPWl = 32 / L.W, NWl = L.NT / 32;
-      const long long rows_w = ceil_div((long long)ceil_div(L.tmax, TPWl) * L.nsteps, NWl);
-      const double gfrac = rows_w > 0 ? 1.0 - (double)L.lam_tail / rows_w : 1.0;
-      if (max_persist > 0 && max_window > 0) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-        cudaStreamAttrValue av = {};
-        av.accessPolicyWindow.base_ptr = pl->d_lam;
-        av.accessPolicyWindow.num_bytes = std::min(used, (size_t)max_window);
-        av.accessPolicyWindow.hitRatio =
-            (float)std::min(1.0, (double)max_persist / std::max(1.0, gfrac * av.accessPolicyWindow.num_bytes));
-        if (const char* hr = std::getenv("SWARM_L2_HIT")) av.accessPolicyWindow.hitRatio = (float)std::atof(hr);
-        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
-        cudaGetLastError();
-        if (std::getenv("SWARM_VERBOSE"))
-          std::fprintf(stderr, "[swarm] L2 persisting: max %d B, window max %d B, lambda %zu B, smem rows per warp %d/%lld\n",
-                       max_persist, max_window, used, L.lam_tail, rows_w);
-      }
-    }
   } else {
     k.lam_ws = nullptr;
   }
@@ -468,14 +446,63 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   cfg.blockDim = dim3(L.NT);
   cfg.dynamicSmemBytes = L.smem_bytes;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = L.C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[3];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = L.C;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
+  // Multi-cluster launches (grid barrier per iteration) need all their CTAs resident at once.
+  // The launch is sized from cudaOccupancyMaxActiveClusters, and kernels that do not wait on
+  // anyone (batches, other solves) always retire, so the only in-process deadlock is two
+  // grid-barrier launches each holding SMs the other waits for: they are serialized
+  // device-wide here.  (cudaLaunchAttributeCooperative would also guarantee residency but
+  // measured 5-8x slower per iteration on B200 with clusters: DESIGN.md §4.)  A barrier that
+  // still never completes (another process) ends in a trap after 30 s, not a hung device.
+  cudaEvent_t multi_ev = nullptr;
+  std::unique_lock<std::mutex> multi_lock;
+  if (L.K > 1) {
+    multi_lock = std::unique_lock<std::mutex>(g_multi_mu);
+    multi_ev = multi_event(pl->device);
+    if (!multi_ev) return fail(ST_ECUDA, "cannot create the multi-cluster ordering event");
+    ST_CUDA(cudaStreamWaitEvent(s, multi_ev, 0));
+  }
+  if (!L.lam_smem) {
+    // keep the multiplier slabs resident in L2 (persisting window), for this launch only
+    const char* pe = std::getenv("SWARM_L2_PERSIST");
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, pl->device);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, pl->device);
+    if ((!pe || std::atoi(pe) != 0) && max_persist > 0 && max_window > 0) {
+      if (!pl->persist_set) {
+        // device-wide carve-out for persisting lines (set once per plan's device)
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+        cudaGetLastError();
+        pl->persist_set = 1;
+      }
+      const size_t used = (size_t)L.nclusters * L.C * L.lam_per_cta * esize;
+      const int TPWl = 32 / L.W, NWl = L.NT / 32;
+      const long long rows_w = ceil_div((long long)ceil_div(L.tmax, TPWl) * L.nsteps, NWl);
+      const double gfrac = rows_w > 0 ? 1.0 - (double)L.lam_tail / rows_w : 1.0;
+      at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[na].val.accessPolicyWindow.base_ptr = pl->d_lam;
+      at[na].val.accessPolicyWindow.num_bytes = std::min(used, (size_t)max_window);
+      at[na].val.accessPolicyWindow.hitRatio =
+          (float)std::min(1.0, (double)max_persist / std::max(1.0, gfrac * at[na].val.accessPolicyWindow.num_bytes));
+      if (const char* hr = std::getenv("SWARM_L2_HIT")) at[na].val.accessPolicyWindow.hitRatio = (float)std::atof(hr);
+      at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      ++na;
+    }
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   ST_CUDA(cudaLaunchKernelEx(&cfg, L.fn, k));
+  if (multi_ev) ST_CUDA(cudaEventRecord(multi_ev, s));
+  // launches sharing this plan's workspaces (counter, slabs, exchange buffers) run in order,
+  // whatever streams their callers use (advice r1: st_solve_device on several streams)
+  ST_CUDA(cudaEventRecord(pl->ev_done, s));
   if (timers) {
     std::vector<long long> h(256 * 16);
     ST_CUDA(cudaMemcpyAsync(h.data(), d_ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
@@ -514,6 +541,7 @@ int check_common(st_plan* pl, int batch, int switch_every, int max_iters, double
   if (max_iters < 1) return fail(ST_EINVAL, "max_iters must be >= 1");
   if (!(tol > 0)) return fail(ST_EINVAL, "tolerance must be positive");
   if ((flags & ST_FLAG_KEEP_STATE) && batch != 1) return fail(ST_EINVAL, "keep_state needs batch == 1");
+  if (flags & ~(ST_FLAG_KEEP_STATE | ST_FLAG_FP32)) return fail(ST_EINVAL, "unknown flag bits");
   return 0;
 }
 
@@ -606,6 +634,7 @@ int st_plan_create(int n, int nobs, int m, int nv, int S, const double* P, const
   if (e == cudaSuccess) e = cudaMalloc(&pl->d_counter, sizeof(int));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&pl->ev[i]);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pl->ev_done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&pl->smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   if (e != cudaSuccess) {
@@ -632,6 +661,10 @@ int st_plan_destroy(st_plan* pl) {
   if (pl->stream) cudaStreamSynchronize(pl->stream);
   for (auto& e : pl->ev)
     if (e) cudaEventDestroy(e);
+  if (pl->ev_done) {
+    cudaEventSynchronize(pl->ev_done);
+    cudaEventDestroy(pl->ev_done);
+  }
   if (pl->d_mats) cudaFree(pl->d_mats);
   if (pl->d_counter) cudaFree(pl->d_counter);
   if (pl->d_lam) cudaFree(pl->d_lam);
@@ -643,12 +676,12 @@ int st_plan_destroy(st_plan* pl) {
   return ST_OK;
 }
 
-int st_query_launch(st_plan* pl, int batch, int hint, long long* out8) {
+int st_query_launch(st_plan* pl, int batch, int hint, int flags, long long* out8) {
   if (!pl || !out8 || batch < 1) return fail(ST_EINVAL, "bad arguments");
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  int rc = choose_launch(pl, batch, hint, false, L);
+  int rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, 1, (flags & ST_FLAG_FP32) != 0);
   if (rc) return rc;
   out8[0] = L.C; out8[1] = L.NB; out8[2] = L.W; out8[3] = L.NT;
   out8[4] = L.lam_smem; out8[5] = (long long)L.smem_bytes; out8[6] = L.nclusters; out8[7] = L.nsteps;
@@ -665,7 +698,7 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L);
+  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, 1, (flags & ST_FLAG_FP32) != 0);
   if (rc) return rc;
   cudaStream_t s = stream ? (cudaStream_t)stream : pl->stream;
   return run(pl, L, batch, c0, beq, geom, switch_every, max_iters, tol, flags, c_out, hist, iters, conv, lam_out,
@@ -683,7 +716,8 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
   Launch L;
-  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, ext ? ext->G : 1);
+  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, ext ? ext->G : 1,
+                     (flags & ST_FLAG_FP32) != 0);
   if (rc) return rc;
   const int n = pl->n, nv = pl->nv, m = pl->m;
   const long long p = (long long)n * (n - 1) / 2 + (long long)n * pl->nobs;

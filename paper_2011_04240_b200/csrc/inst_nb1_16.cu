@@ -3,7 +3,7 @@
 #include "am_kernel.cuh"
 
 namespace swarm {
-template __global__ void am_cluster_kernel<1, 512, 16, 0, 1>(const KParams);
-template __global__ void am_cluster_kernel<1, 512, 16, 1, 1>(const KParams);
-template __global__ void am_cluster_kernel<1, 512, 16, 2, 1>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 16, 0, false>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 16, 1, false>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 16, 2, false>(const KParams);
 }  // namespace swarm

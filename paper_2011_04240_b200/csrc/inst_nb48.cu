@@ -3,8 +3,8 @@
 #include "am_kernel.cuh"
 
 namespace swarm {
-template __global__ void am_cluster_kernel<4, 256, 12, 1, 1>(const KParams);
-template __global__ void am_cluster_kernel<4, 256, 12, 2, 1>(const KParams);
-template __global__ void am_cluster_kernel<8, 256, 12, 1, 1>(const KParams);
-template __global__ void am_cluster_kernel<8, 256, 12, 2, 1>(const KParams);
+template __global__ void am_cluster_kernel<4, 256, 12, 1, false>(const KParams);
+template __global__ void am_cluster_kernel<4, 256, 12, 2, false>(const KParams);
+template __global__ void am_cluster_kernel<8, 256, 12, 1, false>(const KParams);
+template __global__ void am_cluster_kernel<8, 256, 12, 2, false>(const KParams);
 }  // namespace swarm

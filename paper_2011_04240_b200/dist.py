@@ -108,20 +108,23 @@ def am_solve_pair_sharded(spec, config=None, cache=None, group=None, shard_group
     if config.track_descent or config.keep_state:
         raise NotImplementedError("pair-sharded solves support neither track_descent nor keep_state")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    if config.device is None or (config.device == 0 and "LOCAL_RANK" in os.environ):
+    dev = engine._opt(config, "device", None)
+    if dev is None or (dev == 0 and "LOCAL_RANK" in os.environ):
         config = _with_device(config, int(os.environ.get("LOCAL_RANK", 0)))
     v = validate(spec)
     if v:
-        raise engine.InfeasibleProblemError(v)
+        raise engine._infeasible(v)
     t0 = time.perf_counter()
     n, n_obs = len(spec.start), len(spec.obstacles)
     basis = poly.for_spec(spec)
     fp = kkt.fingerprint(basis, n, n_obs)
     c0, beq, geom = engine.pack([spec], basis)
     t1 = time.perf_counter()
-    cache = cache if cache is not None else engine.default_cache()
+    cache, foreign = engine._resolve_cache(cache)
     schedule = config.schedule()
+    before = cache.stats()
     plan = engine._plan_for(cache, fp, basis, schedule, n, n_obs, config.device)
+    engine._sync_foreign(cache, foreign, before)
     own = shard_group is None
     sg = ShardGroup(plan, rank, world, group) if own else shard_group
     try:
@@ -135,14 +138,24 @@ def am_solve_pair_sharded(spec, config=None, cache=None, group=None, shard_group
     if rank != 0:
         return None
     out = dict(out, lam=None, d=None)
-    rep = engine._make_reports([spec], out, basis, plan, cache, schedule, config, (t0, t1, t2, t3))[0]
+    rep = engine._make_reports([spec], out, basis, plan, cache, schedule, config, (t0, t1, t2, t3),
+                               foreign=foreign)[0]
     rep.timings["pair_shards"] = world
     return rep
 
 
+class _DeviceConfig:
+    """A solver config (ours or the reference's) seen with a different device ordinal."""
+
+    def __init__(self, config, device: int):
+        self._config, self.device = config, device
+
+    def __getattr__(self, name):
+        return getattr(self._config, name)
+
+
 def _with_device(config, device: int):
-    import dataclasses
-    return dataclasses.replace(config, device=device)
+    return _DeviceConfig(config, device)
 
 
 def pair_shard_samples(m: int, world: int, cluster: int, clusters_per_gpu: int) -> list[tuple[int, int]]:

@@ -20,7 +20,9 @@ from __future__ import annotations
 
 import logging
 import math
+import sys
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -31,6 +33,11 @@ from .spec import obstacle_axes, validate
 log = logging.getLogger(__name__)
 
 
+class NonFiniteStateError(AssertionError):
+    """The pair state left its valid range (NaN/inf), where the reference's ``_check_ranges``
+    assertion fires (solver.py:355-360, called every iteration at solver.py:437)."""
+
+
 class InfeasibleProblemError(ValueError):
     def __init__(self, violations):
         self.violations = list(violations)
@@ -38,6 +45,32 @@ class InfeasibleProblemError(ValueError):
         if len(self.violations) > 5:
             text += f"; ... ({len(self.violations)} total)"
         super().__init__(f"invalid problem instance: {text}")
+
+
+def _infeasible(violations) -> InfeasibleProblemError:
+    """The validation error to raise.  When the reference package is loaded (the drop-in is
+    serving its callers, cli.py:186-191 / app.py:70-86 catch ``swarmtraj.InfeasibleProblemError``),
+    the error is an instance of both classes so either ``except`` clause catches it."""
+    ref = sys.modules.get("swarmtraj.solver")
+    ref_cls = getattr(ref, "InfeasibleProblemError", None)
+    if isinstance(ref_cls, type) and issubclass(ref_cls, ValueError) and ref_cls is not InfeasibleProblemError:
+        both = _COMPAT_ERRORS.get(ref_cls)
+        if both is None:
+            both = type("InfeasibleProblemError", (InfeasibleProblemError, ref_cls), {})
+            _COMPAT_ERRORS[ref_cls] = both
+        err = both.__new__(both)
+        InfeasibleProblemError.__init__(err, violations)
+        return err
+    return InfeasibleProblemError(violations)
+
+
+_COMPAT_ERRORS: dict = {}
+
+
+def _opt(config, name: str, default):
+    """B200 extension fields of SolverConfig; the reference's own config (schemas.py:88-89,
+    solver.py:60-82) has none of them and gets the defaults."""
+    return getattr(config, name, default)
 
 
 @dataclass
@@ -50,9 +83,11 @@ class SolverConfig:
     initialization: str = "straight_line"
     track_descent: bool = False
     keep_state: bool = False
-    # B200 extensions (not in the reference): CTAs per scenario (0 = auto), device ordinal
+    # B200 extensions (not in the reference): CTAs per scenario (0 = auto), device ordinal,
+    # FP32 pair state (multipliers and pair arithmetic in FP32, FP64 solve)
     cluster_size: int = 0
     device: int = 0
+    fp32: bool = False
 
     def __post_init__(self):
         if self.max_iters < 1:
@@ -83,6 +118,64 @@ class Multipliers:
         return (self.lambda_x, self.lambda_y, self.lambda_z)[axis]
 
 
+class PairRows:
+    """Host view of the pair incidence of one spec -- the attributes of the reference's
+    ``PairwiseBlock`` (kkt_cache.py:104-135) that its state functions read (``apply``,
+    ``apply_transpose``, ``offsets``, ``l_xy``, ``l_z``, ``num_pairs``, ``basis``), so the
+    reference's ``update_multipliers`` / ``compute_residual`` / ``augmented_cost``
+    (solver.py:228-303) run on a ``keep_state`` export.  Rows: agent pairs (i<j,
+    lexicographic), then (agent, obstacle) agent-major (kkt_cache.py:197-215).  Diagnostic
+    only, never on the solve path."""
+
+    def __init__(self, spec, basis):
+        n, n_obs = len(spec.start), len(spec.obstacles)
+        self.basis, self.num_agents = basis, n
+        self._ii, self._jj = np.triu_indices(n, k=1)
+        npair = len(self._ii)
+        self.num_pairs = npair + n * n_obs
+        self.offsets = np.zeros((self.num_pairs, 3))
+        self.l_xy = np.full(self.num_pairs, float(spec.geometry.l_xy))
+        self.l_z = np.full(self.num_pairs, float(spec.geometry.l_z))
+        self._obs_agent = np.repeat(np.arange(n), n_obs)
+        for i in range(n):
+            for k, obs in enumerate(spec.obstacles):
+                row = npair + i * n_obs + k
+                self.offsets[row] = obs.center
+                self.l_xy[row], self.l_z[row] = obstacle_axes(spec, obs)
+
+    def apply(self, c_flat: np.ndarray) -> np.ndarray:
+        """(n * n_v,) coefficients of one axis -> (p * m,) pair differences, pair-major."""
+        X = c_flat.reshape(self.num_agents, -1) @ self.basis.P.T
+        return np.concatenate([X[self._ii] - X[self._jj], X[self._obs_agent]]).ravel()
+
+    def apply_transpose(self, v: np.ndarray) -> np.ndarray:
+        """(p * m,) -> (n * n_v,): (S' v) P."""
+        v = v.reshape(self.num_pairs, -1)
+        acc = np.zeros((self.num_agents, v.shape[1]))
+        npair = len(self._ii)
+        np.add.at(acc, self._ii, v[:npair])
+        np.add.at(acc, self._jj, -v[:npair])
+        np.add.at(acc, self._obs_agent, v[npair:])
+        return (acc @ self.basis.P).ravel()
+
+
+class SystemView:
+    """``state.system`` of a ``keep_state`` export: ``pairs`` and the smoothness Hessian ``Q``
+    = I (x) Pdd'Pdd (kkt_cache.py:161-235), sparse."""
+
+    def __init__(self, spec, basis):
+        self.pairs = PairRows(spec, basis)
+        self._Q = None
+
+    @property
+    def Q(self):
+        if self._Q is None:
+            import scipy.sparse as sp
+            H = self.pairs.basis.Pddot.T @ self.pairs.basis.Pddot
+            self._Q = sp.kron(sp.identity(self.pairs.num_agents, format="csr"), sp.csr_matrix(H), format="csr")
+        return self._Q
+
+
 @dataclass
 class FinalState:
     """Final solver state exported by ``keep_state`` (reference SolverState, solver.py:107-136)."""
@@ -97,9 +190,17 @@ class FinalState:
     iteration: int
     residual_norms: list
     residual_max: list
+    system: SystemView | None = None
 
     def coeffs(self, axis: int) -> np.ndarray:
         return (self.c_x, self.c_y, self.c_z)[axis]
+
+    def set_coeffs(self, axis: int, value: np.ndarray) -> None:
+        setattr(self, ("c_x", "c_y", "c_z")[axis], value)
+
+    def sampled_positions(self) -> np.ndarray:
+        P = self.system.pairs.basis.P
+        return np.stack([self.coeffs(a) @ P.T for a in range(3)], axis=-1)
 
 
 @dataclass
@@ -179,7 +280,45 @@ def pack(specs, basis: poly.Basis):
 
 def _plan_for(cache: kkt.FactorCache, fp, basis, schedule, n, n_obs, device):
     ops = cache.prefactorize(fp, basis, schedule)
-    return cache.plan(fp, schedule, lambda: native.Plan(n, n_obs, basis, ops, device=device))
+    return cache.plan(fp, schedule, lambda: native.Plan(n, n_obs, basis, ops, device=device), device=device)
+
+
+# Reference FactorCache objects (kkt_cache.py:385-456) passed in by the reference's callers
+# (cli.py:209, bench.py:101, app.py:77): their LU store is useless to the device path, so the
+# stage operators and device plans live in a side cache tied to the caller's object, and the
+# caller's counters are advanced exactly as the reference would advance them.
+_SIDE_CACHES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_SIDE_LOCK = __import__("threading").Lock()
+
+
+def _resolve_cache(cache):
+    """-> (our FactorCache, foreign reference cache or None)."""
+    if cache is None:
+        return default_cache(), None
+    if isinstance(cache, kkt.FactorCache):
+        return cache, None
+    if not all(hasattr(cache, a) for a in ("factorizations", "hits", "misses", "solves", "stats")):
+        raise TypeError(f"cache must be a FactorCache, got {type(cache).__name__}")
+    with _SIDE_LOCK:
+        side = _SIDE_CACHES.get(cache)
+        if side is None:
+            side = kkt.FactorCache(disk_dir=getattr(cache, "disk_dir", None))
+            _SIDE_CACHES[cache] = side
+            ref_stats = cache.stats
+            # reference stats() counts its LU entries; add the device-side stage entries
+            cache.stats = lambda: {**ref_stats(), "entries": ref_stats()["entries"] + side.stats()["entries"]}
+    return side, cache
+
+
+def _sync_foreign(side: kkt.FactorCache, foreign, before: dict) -> None:
+    """Advance the reference cache's counters by what the side cache just did."""
+    if foreign is None:
+        return
+    after = side.stats()
+    lock = getattr(foreign, "_lock", None)
+    with (lock if lock is not None else _SIDE_LOCK):
+        for k in ("factorizations", "hits", "misses", "solves"):
+            setattr(foreign, k, getattr(foreign, k) + after[k] - before[k])
 
 
 def _check_batch(specs):
@@ -251,7 +390,7 @@ def _descent_slack(spec, basis, plan, c0, beq, geom, schedule, config, iteration
     states = {}
     for k in range(1, iterations):
         out = plan.solve(c0, beq, geom, schedule.switch_every, k, config.tolerance, keep_state=True,
-                         cluster_hint=config.cluster_size)
+                         cluster_hint=_opt(config, "cluster_size", 0), fp32=_opt(config, "fp32", False))
         _, _, _, alpha, beta = _pair_state(spec, out["c"][0], basis)
         states[k] = (out["c"][0], alpha, beta, out["d"], out["lam"])
     for k in range(1, iterations):
@@ -268,7 +407,8 @@ def _descent_slack(spec, basis, plan, c0, beq, geom, schedule, config, iteration
     return slack
 
 
-def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with_metrics=True) -> list:
+def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with_metrics=True,
+                  foreign=None) -> list:
     """Device outputs of one launch -> one SolveReport per scenario (reference field layout)."""
     t0, t1, t2, t3 = stamps
     h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
@@ -279,16 +419,18 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
     PT = basis.P.T
     trajs = np.stack([np.stack([c[a] @ PT for a in range(3)], axis=-1) for c in out["c"]])
     tc0 = time.perf_counter()
-    cols = (metrics.collision_summary_device_batch(trajs, specs, config.device) if with_metrics
+    cols = (metrics.collision_summary_device_batch(trajs, specs, _opt(config, "device", 0)) if with_metrics
             else [None] * len(specs))
     col_s = (time.perf_counter() - tc0) / len(specs)
     for b, spec in enumerate(specs):
         it = int(out["iters"][b])
+        before = cache.stats()
         cache.count_solve(3 * it)
+        _sync_foreign(cache, foreign, before)
         coeffs = out["c"][b]
         traj = trajs[b]
         tm0 = time.perf_counter()
-        rep_metrics = (metrics.final_metrics(spec, traj, device=config.device, collisions=cols[b])
+        rep_metrics = (metrics.final_metrics(spec, traj, device=_opt(config, "device", 0), collisions=cols[b])
                        if with_metrics else {})
         hist = out["hist"][b]
         timings = {
@@ -313,7 +455,8 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
                 pair_vars=PairVariables(alpha=alpha, beta=beta, d=out["d"]),
                 multipliers=Multipliers(lambda_x=lam[0], lambda_y=lam[1], lambda_z=lam[2]),
                 rho=schedule.values[stage], stage=stage, iteration=it,
-                residual_norms=list(hist[0, :it]), residual_max=list(hist[1, :it]))
+                residual_norms=list(hist[0, :it]), residual_max=list(hist[1, :it]),
+                system=SystemView(spec, basis))
         reports.append(SolveReport(
             trajectories=traj,
             coefficients=coeffs,
@@ -326,7 +469,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
             boundary_max_history=[float(v) for v in hist[2, :it]],
             timings=timings,
             metrics=rep_metrics,
-            cache_stats=cache.stats(),
+            cache_stats=(foreign if foreign is not None else cache).stats(),
             diagnostics=diagnostics,
         ))
     return reports
@@ -344,7 +487,7 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
     for spec in specs:
         v = validate(spec)
         if v:
-            raise InfeasibleProblemError(v)
+            raise _infeasible(v)
     _check_batch(specs)
     if config.keep_state and len(specs) != 1:
         raise ValueError("keep_state is only available for single solves")
@@ -355,14 +498,23 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
     fp = kkt.fingerprint(basis, n, n_obs)
     c0, beq, geom = pack(specs, basis)
     t1 = time.perf_counter()
-    cache = cache if cache is not None else default_cache()
+    cache, foreign = _resolve_cache(cache)
     schedule = config.schedule()
-    plan = _plan_for(cache, fp, basis, schedule, n, n_obs, config.device)
+    before = cache.stats()
+    plan = _plan_for(cache, fp, basis, schedule, n, n_obs, _opt(config, "device", 0))
+    _sync_foreign(cache, foreign, before)
     t2 = time.perf_counter()
     out = plan.solve(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
-                     keep_state=config.keep_state, cluster_hint=config.cluster_size)
+                     keep_state=config.keep_state, cluster_hint=_opt(config, "cluster_size", 0),
+                     fp32=_opt(config, "fp32", False))
     t3 = time.perf_counter()
-    reports = _make_reports(specs, out, basis, plan, cache, schedule, config, (t0, t1, t2, t3), with_metrics)
+    bad = np.flatnonzero(out["status"] == native.ST_NONFINITE)
+    if bad.size:
+        raise NonFiniteStateError(
+            f"non-finite pair state (d/beta out of range) in iteration {int(out['iters'][bad[0]])} of scenario "
+            f"{int(bad[0])}" + (f" and {bad.size - 1} more scenario(s)" if bad.size > 1 else ""))
+    reports = _make_reports(specs, out, basis, plan, cache, schedule, config, (t0, t1, t2, t3), with_metrics,
+                            foreign=foreign)
     if config.track_descent:
         reports[0].diagnostics["descent_slack"] = _descent_slack(
             spec0, basis, plan, c0, beq, geom, schedule, config, reports[0].iterations, reports[0].coefficients)

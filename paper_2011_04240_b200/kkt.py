@@ -290,9 +290,9 @@ class FactorCache:
         manifest["bytes"] = (entry / OPERATORS_FILE).stat().st_size
         return manifest
 
-    def plan(self, fp: Fingerprint, schedule: RhoSchedule, build):
-        """Device plan for (fingerprint, rho values), created once via ``build()``."""
-        key = (fp.key(), tuple(float(v) for v in schedule.values))
+    def plan(self, fp: Fingerprint, schedule: RhoSchedule, build, device: int = 0):
+        """Device plan for (fingerprint, rho values, device ordinal), created once via ``build()``."""
+        key = (fp.key(), tuple(float(v) for v in schedule.values), int(device))
         with self._lock:
             plan = self._plans.get(key)
         if plan is not None:

@@ -19,6 +19,9 @@ from . import poly
 LIB_PATH = os.environ.get("SWARM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_swarm_am.so")
 
 ST_FLAG_KEEP_STATE = 1
+ST_FLAG_FP32 = 2
+# per-scenario status in the ``converged`` output: 1 converged, 0 not, -1 non-finite state
+ST_NONFINITE = -1
 _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedError}
 
 EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
@@ -50,7 +53,7 @@ def load() -> ctypes.CDLL:
         lib.st_solve.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip, _dp, _dp,
                                  ctypes.POINTER(ctypes.c_float)]
         lib.st_solve_device.argtypes = [vp, i, vp, vp, vp, i, i, d, i, i, vp, vp, vp, vp, vp, vp, vp]
-        lib.st_query_launch.argtypes = [vp, i, i, ctypes.POINTER(ctypes.c_longlong)]
+        lib.st_query_launch.argtypes = [vp, i, i, i, ctypes.POINTER(ctypes.c_longlong)]
         lib.st_last_error.restype = ctypes.c_char_p
         ub = ctypes.POINTER(ctypes.c_ubyte)
         lib.st_shard_layout.argtypes = [vp, i, ctypes.POINTER(ctypes.c_longlong)]
@@ -117,15 +120,16 @@ class Plan:
     def num_pairs(self) -> int:
         return self.n * (self.n - 1) // 2 + self.n * self.n_obs
 
-    def query_launch(self, batch: int = 1, cluster_hint: int = 0) -> dict:
+    def query_launch(self, batch: int = 1, cluster_hint: int = 0, fp32: bool = False, keep_state: bool = False) -> dict:
         out = (ctypes.c_longlong * 8)()
-        _check(self._lib.st_query_launch(self._h, batch, cluster_hint, out))
+        flags = (ST_FLAG_FP32 if fp32 else 0) | (ST_FLAG_KEEP_STATE if keep_state else 0)
+        _check(self._lib.st_query_launch(self._h, batch, cluster_hint, flags, out))
         keys = ("cluster", "agent_blocks", "lane_width", "threads", "lambda_in_smem", "smem_bytes",
                 "clusters", "steps_per_task")
         return dict(zip(keys, (int(v) for v in out)))
 
     def solve(self, c0, beq, geom, switch_every: int, max_iters: int, tol: float,
-              keep_state: bool = False, cluster_hint: int = 0, out: dict | None = None) -> dict:
+              keep_state: bool = False, cluster_hint: int = 0, out: dict | None = None, fp32: bool = False) -> dict:
         """Host-buffer solve of a batch: c0 (B,3,n,nv), beq (B,3,n,6), geom (B, 2+5 n_obs).
 
         ``out`` may supply preallocated (e.g. page-locked) output arrays: ``c`` (B,3,n,nv)
@@ -156,18 +160,19 @@ class Plan:
             d = np.empty((self.num_pairs, self.m))
         t = (ctypes.c_float * 3)()
         _check(self._lib.st_solve(self._h, B, _ptr(c0), _ptr(beq), _ptr(geom), switch_every, max_iters, tol,
-                                  ST_FLAG_KEEP_STATE if keep_state else 0, cluster_hint, _ptr(c_out),
+                                  (ST_FLAG_KEEP_STATE if keep_state else 0) | (ST_FLAG_FP32 if fp32 else 0),
+                                  cluster_hint, _ptr(c_out),
                                   _ptr(hist), _ptr(iters, _ip), _ptr(conv, _ip), _ptr(lam), _ptr(d), t))
-        return {"c": c_out, "hist": hist, "iters": iters, "converged": conv if out is not None else conv.astype(bool),
-                "lam": lam, "d": d, "timings_ms": tuple(float(x) for x in t)}
+        return {"c": c_out, "hist": hist, "iters": iters, "converged": conv if out is not None else conv > 0,
+                "status": conv.copy(), "lam": lam, "d": d, "timings_ms": tuple(float(x) for x in t)}
 
     def solve_device(self, B: int, c0_ptr: int, beq_ptr: int, geom_ptr: int, switch_every: int,
                      max_iters: int, tol: float, c_out_ptr: int, hist_ptr: int, iters_ptr: int,
-                     conv_ptr: int, stream: int = 0, cluster_hint: int = 0) -> None:
+                     conv_ptr: int, stream: int = 0, cluster_hint: int = 0, fp32: bool = False) -> None:
         """Enqueue a solve on device-resident buffers (raw pointers, e.g. torch ``data_ptr()``)."""
         _check(self._lib.st_solve_device(self._h, B, c0_ptr, beq_ptr, geom_ptr, switch_every, max_iters, tol,
-                                         0, cluster_hint, c_out_ptr, hist_ptr, iters_ptr, conv_ptr, None, None,
-                                         stream or None))
+                                         ST_FLAG_FP32 if fp32 else 0, cluster_hint, c_out_ptr, hist_ptr, iters_ptr,
+                                         conv_ptr, None, None, stream or None))
 
     # ---- pair sharding over GPUs (one process per GPU; see include/swarm_am.h) -------------
 
