@@ -92,11 +92,14 @@ int st_solve_device(st_plan* plan, int batch, const double* c0, const double* b_
 
 /* ---- Pair-sharded solve of ONE large scenario over G GPUs (BASELINE config 5).
  * Replaces nothing in the reference (single process, CPU); it is the north star's
- * "very large n shards the agent pairs across GPUs": every GPU owns a contiguous
- * slice of the time samples (all agent pairs at those samples), the per-iteration
- * exchange of the 3 x n x n_v partial right-hand sides (plus residual norms) goes
- * through peer-mapped buffers inside the one persistent kernel, summed in a fixed
- * participant order (identical on every GPU).  One process per GPU:
+ * "very large n shards the agent pairs across GPUs".  For n > 64 (the large-fleet
+ * kernel) the work units are (agent-block pair x time sample x half) in block-pair-major
+ * order and every GPU owns a contiguous, cost-balanced range of them -- a range of agent
+ * pairs of the upper triangle at all samples -- run by one CTA per SM.  Each GPU reduces
+ * its units to one partial right-hand-side row set (3 x n x n_v doubles) plus its residual
+ * norms; the one per-iteration exchange of those goes through peer-mapped buffers inside
+ * the persistent kernel and is summed in rank order (identical on every GPU).  (n <= 64:
+ * the multi-cluster kernel, every GPU a slice of the time samples.)  One process per GPU:
  *   st_shard_layout  -> cluster size, clusters per GPU, buffer bytes, participants
  *   st_shard_buffer  -> allocate this GPU's buffer and export its IPC handle
  *   st_shard_open    -> map a peer's buffer (cudaIpcOpenMemHandle)
@@ -110,6 +113,12 @@ int st_shard_reset(st_plan* plan, void* buf0);
 int st_solve_sharded(st_plan* plan, int G, int rank, void* const* bufs, const double* c0, const double* b_eq,
                      const double* geom, int switch_every, int max_iters, double tol, double* c_out,
                      double* hist, int* iters, int* converged, float* timings_ms);
+
+/* Host-only (no device needed): the large-fleet unit partition for n agents, m samples,
+ * G GPUs of cpg CTAs.  Fills (when non-NULL) u_range[G+1] (GPU g owns units
+ * [u_range[g], u_range[g+1])), cta_first[G*(cpg+1)], rows[U] (pair steps per unit) and
+ * ab_first[nab+1] (first unit of each agent-block pair); returns U, the unit count. */
+int st_large_partition(int n, int m, int G, int cpg, int* u_range, int* cta_first, int* rows, int* ab_first);
 
 /* Launch configuration st_solve would use (flags as for st_solve): out[0..7] =
  * cluster size C, agent blocks NB, lane segment width W, threads per CTA,

@@ -13,6 +13,7 @@
 #include "../../include/swarm_am.h"
 #define SWARM_KERNEL_DECL_ONLY
 #include "am_kernel.cuh"
+#include "am_large.cuh"
 
 namespace {
 
@@ -82,7 +83,7 @@ struct st_plan {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int* d_counter = nullptr;
-  double* d_lam = nullptr;
+  double* d_lam = nullptr;  // multiplier slabs (double or float elements)
   size_t lam_bytes = 0;
   double* d_cws = nullptr;
   size_t c_bytes = 0;
@@ -94,6 +95,9 @@ struct st_plan {
   int smem_sm = 0;  // shared memory per SM
   int persist_set = 0;
   cudaEvent_t ev_done = nullptr;  // last launch that used this plan's workspaces
+  void* d_lgw = nullptr;          // large-fleet workspace (tables, unit slots, positions, ...)
+  size_t lgw_bytes = 0;
+  std::vector<long long> lg_key;  // layout whose tables are in d_lgw
   std::mutex mu;
 };
 
@@ -352,6 +356,101 @@ struct ShardExt {
   void* bufs[8];
 };
 
+// ---------------------------------------------------------------------------------------------
+// Large fleets (am_large.cuh): one scenario over every SM (and over G GPUs when pair-sharded)
+
+using LargeFn = void (*)(swarm::LgParams);
+struct LargeEntry {
+  int NVMAX;
+  bool f32;
+  LargeFn fn;
+};
+const LargeEntry kLarge[] = {
+    {12, false, swarm::am_large_kernel<12, false>}, {12, true, swarm::am_large_kernel<12, true>},
+    {16, false, swarm::am_large_kernel<16, false>}, {16, true, swarm::am_large_kernel<16, true>},
+};
+
+bool large_eligible(const st_plan* pl, int batch, bool keep) {
+  const char* e = std::getenv("SWARM_LARGE");
+  const int mode = e ? std::atoi(e) : 1;
+  if (mode == 0 || batch != 1 || keep || pl->nobs != 0 || pl->n < 2 || pl->n > 32 * swarm::LG_MAXB) return false;
+  return mode == 2 || pl->n > 64;
+}
+
+// Units in block-pair-major order: a diagonal block pair (A == B) has one unit per sample t
+// (u = ab_first[ab] + t), a cross pair two (u = ab_first[ab] + 2 t + h); pair-step rows of each.
+struct LargeLayout {
+  int NB = 0, nab = 0, npad = 0, m = 0, U = 0, G = 1, cpg = 0;
+  std::vector<int> ab;         // nab x 2
+  std::vector<int> ab_first;   // nab + 1
+  std::vector<int> rows;       // U
+  std::vector<int> u_range;    // G + 1
+  std::vector<int> cta_first;  // G x (cpg + 1)
+};
+
+LargeLayout large_layout(const st_plan* pl, int G, int cpg) {
+  LargeLayout Lg;
+  const int n = pl->n;
+  Lg.NB = (n + 31) / 32;
+  Lg.npad = Lg.NB * 32;
+  Lg.m = pl->m;
+  for (int A = 0; A < Lg.NB; ++A)
+    for (int B = A; B < Lg.NB; ++B) { Lg.ab.push_back(A); Lg.ab.push_back(B); }
+  Lg.nab = (int)Lg.ab.size() / 2;
+  Lg.ab_first.assign(Lg.nab + 1, 0);
+  for (int ab = 0; ab < Lg.nab; ++ab) Lg.ab_first[ab + 1] = Lg.ab_first[ab] + (Lg.ab[2 * ab] == Lg.ab[2 * ab + 1] ? 1 : 2) * Lg.m;
+  Lg.U = Lg.ab_first[Lg.nab];
+  Lg.rows.resize(Lg.U);
+  std::vector<long long> pre(Lg.U + 1, 0);
+  for (int ab = 0; ab < Lg.nab; ++ab) {
+    const int A = Lg.ab[2 * ab], B = Lg.ab[2 * ab + 1];
+    const int nA = std::min(32, n - 32 * A);
+    for (int u = Lg.ab_first[ab]; u < Lg.ab_first[ab + 1]; ++u) Lg.rows[u] = (A == B) ? nA / 2 : swarm::LG_UNIT_STEPS;
+  }
+  for (int u = 0; u < Lg.U; ++u) pre[u + 1] = pre[u] + Lg.rows[u];
+  // contiguous cost-balanced ranges: the first unit whose prefix cost reaches the target
+  auto cut = [&](long long target) {
+    return (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+  };
+  Lg.G = G;
+  Lg.cpg = cpg;
+  const long long T = pre[Lg.U];
+  Lg.u_range.resize(G + 1);
+  for (int g = 0; g <= G; ++g) Lg.u_range[g] = g == G ? Lg.U : cut(T * g / G);
+  Lg.cta_first.resize((size_t)G * (cpg + 1));
+  for (int g = 0; g < G; ++g) {
+    const long long c0 = pre[Lg.u_range[g]], c1 = pre[Lg.u_range[g + 1]];
+    for (int c = 0; c <= cpg; ++c)
+      Lg.cta_first[(size_t)g * (cpg + 1) + c] =
+          c == cpg ? Lg.u_range[g + 1] : std::max(Lg.u_range[g], cut(c0 + (c1 - c0) * c / cpg));
+  }
+  return Lg;
+}
+
+// CTAs per SM the large kernel fits (1 by design), and the grid of one GPU
+int large_grid(st_plan* pl, const LargeEntry* le, size_t smem, int& grid) {
+  ST_CUDA(cudaFuncSetAttribute(le->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0, nsm = 0;
+  ST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, le->fn, swarm::LG_NT, smem));
+  ST_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device));
+  if (occ < 1) return fail(ST_EUNSUPPORTED, "large-fleet kernel does not fit on an SM");
+  grid = occ * nsm;
+  if (const char* e = std::getenv("SWARM_LARGE_GRID")) grid = std::max(1, std::min(grid, std::atoi(e)));
+  return 0;
+}
+
+// Growable device workspace owned by the plan (freed and reallocated only when it must grow;
+// the plan's launch ordering event makes reuse safe).
+int grow(void** ptr, size_t* cap, size_t need) {
+  if (need <= *cap) return 0;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  ST_CUDA(cudaMalloc(ptr, need));
+  *cap = need;
+  return 0;
+}
+
 int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double* beq, const double* geom,
         int switch_every, int max_iters, double tol, int flags, double* c_out, double* hist, int* iters,
         int* conv, double* lam_out, double* d_out, cudaStream_t s, const ShardExt* ext = nullptr) {
@@ -534,6 +633,183 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   return 0;
 }
 
+// One large scenario through am_large_kernel.  ext != nullptr: this GPU is rank ext->rank of a
+// pair-sharded solve over ext->G GPUs (peer-mapped exchange buffers).  Otherwise
+// SWARM_VIRTUAL_GROUPS=g emulates g ranks inside this one launch (their CTAs wait on one
+// another, so they must share a launch on one GPU).
+int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const double* geom, int switch_every,
+              int max_iters, double tol, double* c_out, double* hist, int* iters, int* conv, cudaStream_t s,
+              const ShardExt* ext) {
+  const LargeEntry* le = nullptr;
+  for (const auto& e : kLarge)
+    if (e.NVMAX == pl->nvmax && e.f32 == f32) le = &e;
+  if (!le) return fail(ST_EUNSUPPORTED, "no large-fleet kernel for this basis degree");
+  const int NV = pl->nvmax;
+  const int chr = swarm::lg_chunk_rows(f32);
+  const swarm::LgSmem sm = NV == 12 ? (f32 ? swarm::lg_smem<12, true>(pl->m, chr) : swarm::lg_smem<12, false>(pl->m, chr))
+                                    : (f32 ? swarm::lg_smem<16, true>(pl->m, chr) : swarm::lg_smem<16, false>(pl->m, chr));
+  const size_t smem = (size_t)sm.total;
+  if ((long long)smem > pl->smem_optin) return fail(ST_EUNSUPPORTED, "large-fleet layout exceeds shared memory");
+  int grid = 0;
+  int rc = large_grid(pl, le, smem, grid);
+  if (rc) return rc;
+  int G = 1, g_base = 0, vgroups = 1;
+  if (ext) {
+    G = ext->G;
+    g_base = ext->rank;
+  } else if (const char* vg = std::getenv("SWARM_VIRTUAL_GROUPS")) {
+    G = vgroups = std::max(1, std::min(8, std::atoi(vg)));
+  }
+  const int cpg = grid / vgroups;
+  if (cpg < 1) return fail(ST_EUNSUPPORTED, "too few SMs for the requested groups");
+  if ((long long)((3 * pl->n + cpg - 1) / cpg) * pl->m * 8 > sm.bar - sm.ring)
+    return fail(ST_EUNSUPPORTED, "large-fleet row reduction does not fit in shared memory");
+  const LargeLayout Lg = large_layout(pl, G, cpg);
+  const int n = pl->n, m = pl->m;
+  // host tables: block pairs, group ranges, CTA ranges, multiplier offsets of this launch's units
+  const int ulo = Lg.u_range[g_base], uhi = Lg.u_range[g_base + vgroups];
+  std::vector<long long> off(uhi - ulo + 1, 0);
+  for (int u = ulo; u < uhi; ++u) off[u - ulo + 1] = off[u - ulo] + 96LL * Lg.rows[u];
+  const size_t esize = f32 ? 4 : 8;
+  const size_t n_ab = Lg.ab.size(), n_af = Lg.ab_first.size(), n_ur = Lg.u_range.size(), n_cf = Lg.cta_first.size();
+  const size_t tab_bytes = ((n_ab + n_af + n_ur + n_cf) * 4 + 15) / 16 * 16 + off.size() * 8;
+  const long long xst = 3LL * n * NV + 4;
+  const size_t q_bytes = (size_t)Lg.U * 192 * 8, x_bytes = (size_t)m * 3 * Lg.npad * 8, cb_bytes = 3ULL * n * NV * 8;
+  const size_t nrm_bytes = (size_t)grid * 16, bnd_bytes = (size_t)vgroups * 16 * 8, bar_bytes = (size_t)(vgroups + 1) * 128;
+  const size_t xch_bytes = (ext || G == 1) ? 0 : (size_t)G * 2 * xst * 8;
+  size_t o = 0;
+  auto carve = [&](size_t bytes) { const size_t r = o; o += (bytes + 255) / 256 * 256; return r; };
+  const size_t o_tab = carve(tab_bytes), o_q = carve(q_bytes), o_x = carve(x_bytes * vgroups),
+               o_cb = carve(cb_bytes * vgroups), o_nrm = carve(nrm_bytes), o_bnd = carve(bnd_bytes),
+               o_bar = carve(bar_bytes), o_xch = carve(xch_bytes);
+  ST_CUDA(cudaStreamWaitEvent(s, pl->ev_done, 0));  // previous launch on this plan has finished
+  rc = grow(&pl->d_lgw, &pl->lgw_bytes, o);
+  if (rc) return rc;
+  rc = grow(reinterpret_cast<void**>(&pl->d_lam), &pl->lam_bytes, std::max<size_t>(16, off.back() * esize));
+  if (rc) return rc;
+  char* base = static_cast<char*>(pl->d_lgw);
+  const std::vector<long long> key = {G, g_base, vgroups, cpg, f32 ? 1 : 0, (long long)pl->d_lgw};
+  if (key != pl->lg_key) {
+    // tables depend only on the layout: uploaded once per layout (pageable copy, synchronized)
+    std::vector<char> h(tab_bytes, 0);
+    std::memcpy(h.data(), Lg.ab.data(), n_ab * 4);
+    std::memcpy(h.data() + n_ab * 4, Lg.ab_first.data(), n_af * 4);
+    std::memcpy(h.data() + (n_ab + n_af) * 4, Lg.u_range.data(), n_ur * 4);
+    std::memcpy(h.data() + (n_ab + n_af + n_ur) * 4, Lg.cta_first.data(), n_cf * 4);
+    std::memcpy(h.data() + tab_bytes - off.size() * 8, off.data(), off.size() * 8);
+    ST_CUDA(cudaMemcpyAsync(base + o_tab, h.data(), tab_bytes, cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaStreamSynchronize(s));  // h is pageable and goes out of scope
+    pl->lg_key = key;
+  }
+  ST_CUDA(cudaMemsetAsync(base + o_bar, 0, bar_bytes, s));
+  swarm::LgParams k{};
+  k.n = n; k.m = m; k.nv = pl->nv; k.S = pl->S; k.NB = Lg.NB; k.nab = Lg.nab; k.npad = Lg.npad;
+  k.P = pl->P; k.mats = pl->mats; k.inv_rho = pl->inv_rho; k.E = pl->E;
+  const int* tab = reinterpret_cast<const int*>(base + o_tab);
+  k.ab_pair = tab;
+  k.ab_first = tab + n_ab;
+  k.u_range = tab + n_ab + n_af;
+  k.cta_first = tab + n_ab + n_af + n_ur;
+  k.lam_off = reinterpret_cast<const long long*>(base + o_tab + tab_bytes - off.size() * 8);
+  k.G = G; k.g_base = g_base; k.vgroups = vgroups; k.cpg = cpg;
+  k.lam = pl->d_lam;
+  k.qbuf = reinterpret_cast<double*>(base + o_q);
+  k.X = reinterpret_cast<double*>(base + o_x);
+  k.cbuf = reinterpret_cast<double*>(base + o_cb);
+  k.x_stride = (long long)(x_bytes / 8);
+  k.c_stride = (long long)(cb_bytes / 8);
+  k.cta_nrm = reinterpret_cast<double*>(base + o_nrm);
+  k.bnd = reinterpret_cast<unsigned long long*>(base + o_bnd);
+  k.gbar = reinterpret_cast<unsigned*>(base + o_bar);
+  k.sysbar = reinterpret_cast<unsigned*>(base + o_bar + (size_t)vgroups * 128);
+  k.sys_scope = 0;
+  for (auto& x : k.xch) x = nullptr;
+  if (ext) {
+    k.sys_scope = 1;
+    k.sysbar = reinterpret_cast<unsigned*>(ext->bufs[0]);
+    for (int g = 0; g < G; ++g) k.xch[g] = reinterpret_cast<double*>(static_cast<char*>(ext->bufs[g]) + 64);
+  } else {
+    for (int g = 0; g < G && G > 1; ++g) k.xch[g] = reinterpret_cast<double*>(base + o_xch) + (size_t)g * 2 * xst;
+  }
+  k.c0 = c0; k.beq = beq; k.geom = geom;
+  k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
+  k.switch_every = switch_every; k.max_iters = max_iters; k.tol = tol;
+  static long long* d_ts = nullptr;
+  const bool timers = std::getenv("SWARM_PHASE_TIMERS") != nullptr;
+  if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 8192 * sizeof(long long)));
+  if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 8192 * sizeof(long long), s));
+  k.tstamp = timers ? d_ts : nullptr;
+  // grid-barrier kernels are serialized device-wide (see run())
+  std::unique_lock<std::mutex> multi_lock(g_multi_mu);
+  cudaEvent_t multi_ev = multi_event(pl->device);
+  if (!multi_ev) return fail(ST_ECUDA, "cannot create the multi-cluster ordering event");
+  ST_CUDA(cudaStreamWaitEvent(s, multi_ev, 0));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cpg * vgroups);
+  cfg.blockDim = dim3(swarm::LG_NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  int na = 0;
+  if (f32 && !std::getenv("SWARM_NO_L2_PERSIST")) {
+    // FP32 multipliers (n = 256: 78 MB) fit in L2: keep them there across iterations
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, pl->device);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, pl->device);
+    if (max_persist > 0 && max_window > 0) {
+      if (!pl->persist_set) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+        cudaGetLastError();
+        pl->persist_set = 1;
+      }
+      const size_t used = off.back() * esize;
+      at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[na].val.accessPolicyWindow.base_ptr = pl->d_lam;
+      at[na].val.accessPolicyWindow.num_bytes = std::min(used, (size_t)max_window);
+      at[na].val.accessPolicyWindow.hitRatio =
+          (float)std::min(1.0, (double)max_persist / std::max<double>(1.0, at[na].val.accessPolicyWindow.num_bytes));
+      at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      ++na;
+    }
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  ST_CUDA(cudaLaunchKernelEx(&cfg, le->fn, k));
+  ST_CUDA(cudaEventRecord(multi_ev, s));
+  ST_CUDA(cudaEventRecord(pl->ev_done, s));
+  if (timers) {
+    std::vector<long long> h(8192);
+    ST_CUDA(cudaMemcpyAsync(h.data(), d_ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    if (std::getenv("SWARM_CTA_TIMES")) {
+      std::fprintf(stderr, "[swarm cta P-phase cycles, iteration 50]");
+      for (int c = 0; c < cpg * vgroups; ++c)
+        std::fprintf(stderr, " %d:%lld(u%d-%d)", c, h[4096 + c], Lg.cta_first[c], Lg.cta_first[c + 1]);
+      std::fprintf(stderr, "\n");
+    }
+    static const char* names[] = {"norms+exchange", "solve+positions", "barrier2", "pairs", "barrier1"};
+    double acc[5] = {0};
+    int cnt = 0;
+    for (int it = 1; it < 255 && h[16 * (it + 1)]; ++it, ++cnt) {
+      const long long* t = &h[16 * it];
+      for (int q = 0; q < 5; ++q) acc[q] += t[q + 1] - t[q];
+    }
+    if (cnt) {
+      std::fprintf(stderr, "[swarm timers] large grid=%d groups=%d iters=%d cycles/iter:", cpg * vgroups, vgroups, cnt);
+      for (int q = 0; q < 5; ++q) std::fprintf(stderr, " %s=%.0f", names[q], acc[q] / cnt);
+      double rs[3] = {0, 0, 0};
+      for (int it = 1; it <= cnt; ++it) {
+        const long long* t = &h[16 * it];
+        if (t[8] && t[9] && t[10]) { rs[0] += t[8] - t[7]; rs[1] += t[9] - t[8]; rs[2] += t[10] - t[9]; }
+      }
+      std::fprintf(stderr, " [cta0: gather=%.0f project=%.0f solve+X=%.0f]", rs[0] / cnt, rs[1] / cnt, rs[2] / cnt);
+      std::fprintf(stderr, "\n");
+    }
+  }
+  return 0;
+}
+
 int check_common(st_plan* pl, int batch, int switch_every, int max_iters, double tol, int flags) {
   if (!pl) return fail(ST_EINVAL, "plan is NULL");
   if (batch < 1) return fail(ST_EINVAL, "batch must be >= 1");
@@ -671,6 +947,7 @@ int st_plan_destroy(st_plan* pl) {
   if (pl->d_cws) cudaFree(pl->d_cws);
   if (pl->d_rg) cudaFree(pl->d_rg);
   if (pl->d_io) cudaFree(pl->d_io);
+  if (pl->d_lgw) cudaFree(pl->d_lgw);
   if (pl->stream) cudaStreamDestroy(pl->stream);
   delete pl;
   return ST_OK;
@@ -697,10 +974,13 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
   if ((flags & ST_FLAG_KEEP_STATE) && (!lam_out || !d_out)) return fail(ST_EINVAL, "keep_state buffers missing");
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : pl->stream;
+  if (hint <= 0 && large_eligible(pl, batch, (flags & ST_FLAG_KEEP_STATE) != 0))
+    return run_large(pl, (flags & ST_FLAG_FP32) != 0, c0, beq, geom, switch_every, max_iters, tol, c_out, hist,
+                     iters, conv, s, nullptr);
   Launch L;
   rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, 1, (flags & ST_FLAG_FP32) != 0);
   if (rc) return rc;
-  cudaStream_t s = stream ? (cudaStream_t)stream : pl->stream;
   return run(pl, L, batch, c0, beq, geom, switch_every, max_iters, tol, flags, c_out, hist, iters, conv, lam_out,
              d_out, s);
 }
@@ -715,10 +995,12 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   if (keep && (!lam_out || !d_out)) return fail(ST_EINVAL, "keep_state buffers missing");
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
+  const bool large = hint <= 0 && large_eligible(pl, batch, keep);
   Launch L;
-  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, ext ? ext->G : 1,
-                     (flags & ST_FLAG_FP32) != 0);
-  if (rc) return rc;
+  if (!large) {
+    rc = choose_launch(pl, batch, hint, keep, L, ext ? ext->G : 1, (flags & ST_FLAG_FP32) != 0);
+    if (rc) return rc;
+  }
   const int n = pl->n, nv = pl->nv, m = pl->m;
   const long long p = (long long)n * (n - 1) / 2 + (long long)n * pl->nobs;
   const size_t n_c = (size_t)batch * 3 * n * nv, n_b = (size_t)batch * 3 * n * 6,
@@ -745,8 +1027,10 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   ST_CUDA(cudaMemcpyAsync(d_beq, beq, n_b * 8, cudaMemcpyHostToDevice, s));
   ST_CUDA(cudaMemcpyAsync(d_geom, geom, n_g * 8, cudaMemcpyHostToDevice, s));
   ST_CUDA(cudaEventRecord(pl->ev[1], s));
-  rc = run(pl, L, batch, d_c0, d_beq, d_geom, switch_every, max_iters, tol, flags, d_cout, d_hist, d_it, d_cv,
-           keep ? d_lam : nullptr, keep ? d_dd : nullptr, s, ext);
+  rc = large ? run_large(pl, (flags & ST_FLAG_FP32) != 0, d_c0, d_beq, d_geom, switch_every, max_iters, tol, d_cout,
+                         d_hist, d_it, d_cv, s, ext)
+             : run(pl, L, batch, d_c0, d_beq, d_geom, switch_every, max_iters, tol, flags, d_cout, d_hist, d_it, d_cv,
+                   keep ? d_lam : nullptr, keep ? d_dd : nullptr, s, ext);
   if (rc) return rc;
   ST_CUDA(cudaEventRecord(pl->ev[2], s));
   ST_CUDA(cudaMemcpyAsync(c_out, d_cout, n_c * 8, cudaMemcpyDeviceToHost, s));
@@ -781,6 +1065,23 @@ int st_shard_layout(st_plan* pl, int G, long long* out4) {
   if (!pl || !out4 || G < 1 || G > 8) return fail(ST_EINVAL, "bad arguments (G must be 1..8)");
   std::lock_guard<std::mutex> g(pl->mu);
   ST_CUDA(cudaSetDevice(pl->device));
+  if (large_eligible(pl, 1, false)) {
+    // large fleets: every GPU runs one CTA per SM over its range of (block pair x sample) units
+    for (const auto& e : kLarge) {
+      if (e.NVMAX != pl->nvmax || e.f32) continue;
+      const int chr = swarm::lg_chunk_rows(false);
+      const swarm::LgSmem sm = pl->nvmax == 12 ? swarm::lg_smem<12, false>(pl->m, chr)
+                                               : swarm::lg_smem<16, false>(pl->m, chr);
+      int grid = 0;
+      int rc = large_grid(pl, &e, (size_t)sm.total, grid);
+      if (rc) return rc;
+      out4[0] = 0;  // no clusters
+      out4[1] = grid;
+      out4[2] = 64 + 2LL * (3LL * pl->n * pl->nvmax + 4) * (long long)sizeof(double);
+      out4[3] = (long long)G * grid;
+      return ST_OK;
+    }
+  }
   Launch L;
   int rc = choose_launch(pl, 1, 0, false, L, G);
   if (rc) return rc;
@@ -790,6 +1091,19 @@ int st_shard_layout(st_plan* pl, int G, long long* out4) {
   out4[2] = 64 + 2LL * L.K * stride * (long long)sizeof(double);
   out4[3] = (long long)L.G * L.K;
   return ST_OK;
+}
+
+int st_large_partition(int n, int m, int G, int cpg, int* u_range, int* cta_first, int* rows, int* ab_first) {
+  if (n < 2 || m < 1 || G < 1 || cpg < 1) return -fail(ST_EINVAL, "bad arguments");
+  st_plan tmp;
+  tmp.n = n;
+  tmp.m = m;
+  const LargeLayout Lg = large_layout(&tmp, G, cpg);
+  if (u_range) std::copy(Lg.u_range.begin(), Lg.u_range.end(), u_range);
+  if (cta_first) std::copy(Lg.cta_first.begin(), Lg.cta_first.end(), cta_first);
+  if (rows) std::copy(Lg.rows.begin(), Lg.rows.end(), rows);
+  if (ab_first) std::copy(Lg.ab_first.begin(), Lg.ab_first.end(), ab_first);
+  return Lg.U;
 }
 
 int st_shard_buffer(st_plan* pl, long long bytes, void** dptr, unsigned char* handle64) {

@@ -27,7 +27,7 @@ _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedErro
 EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
            "st_last_error", "st_version", "st_shard_layout", "st_shard_buffer", "st_shard_open", "st_shard_close",
            "st_shard_reset", "st_solve_sharded", "st_check_collisions",
-           "st_check_collisions_batch")
+           "st_check_collisions_batch", "st_large_partition")
 
 _lib = None
 _lock = threading.Lock()
@@ -67,6 +67,7 @@ def load() -> ctypes.CDLL:
         lib.st_check_collisions.argtypes = [i, i, _dp, d, d, i, _dp, i, ll, _ip, _dp, _dp, ctypes.POINTER(ll)]
         lib.st_check_collisions_batch.argtypes = [i, i, i, _dp, _dp, i, _dp, i, ll, _ip, _dp, _dp,
                                                   ctypes.POINTER(ll)]
+        lib.st_large_partition.argtypes = [i, i, i, i, _ip, _ip, _ip, _ip]
         for name in EXPORTS:
             getattr(lib, name)  # every declared symbol must resolve
         _lib = lib
@@ -284,3 +285,21 @@ def check_collisions_batch(trajs: np.ndarray, geoms: np.ndarray, obs_rows: np.nd
                                      zip(ids_l[e:e + t], vals_l[e:e + t])]))
         e += t
     return out
+
+
+def large_partition(n: int, m: int, groups: int, ctas_per_group: int) -> dict:
+    """Host-only unit partition of the large-fleet kernel (``st_large_partition``)."""
+    lib = load()
+    nb = (n + 31) // 32
+    nab = nb * (nb + 1) // 2
+    U_max = nab * m * 2
+    u_range = np.empty(groups + 1, dtype=np.int32)
+    cta_first = np.empty(groups * (ctas_per_group + 1), dtype=np.int32)
+    rows = np.empty(U_max, dtype=np.int32)
+    ab_first = np.empty(nab + 1, dtype=np.int32)
+    U = lib.st_large_partition(n, m, groups, ctas_per_group, _ptr(u_range, _ip), _ptr(cta_first, _ip),
+                               _ptr(rows, _ip), _ptr(ab_first, _ip))
+    if U < 0:
+        _check(-U)
+    return {"units": int(U), "u_range": u_range, "cta_first": cta_first.reshape(groups, ctas_per_group + 1),
+            "rows": rows[:U], "ab_first": ab_first}

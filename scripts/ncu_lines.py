@@ -8,8 +8,13 @@ rep, lib, kern = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, check=True, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+# the library holds one cubin per translation unit: disassemble the one defining the kernel
+sass = ""
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    if re.search(r"\.text\.\S*" + re.escape(kern), txt):
+        sass = txt
+        break
 addr2line = {}
 cur_fn, cur_line = None, None
 for ln in sass.splitlines():

@@ -157,7 +157,7 @@ def test_chaotic_instances_still_meet_acceptance(cuda_ok):
         assert rep.metrics["min_normalized_distance"] >= 0.95
 
 
-@pytest.mark.parametrize("name", ["rand48_s0", "rand20_s0", "obs8", "circ16j"])
+@pytest.mark.parametrize("name", ["rand48_s0", "rand20_s0", "obs8", "circ16j", "rand128_s0"])
 def test_results_independent_of_stale_device_memory(cuda_ok, name):
     """Poison freed device memory with NaN bit patterns first: no kernel may read a slot it did not write."""
     import torch
@@ -173,10 +173,11 @@ def test_results_independent_of_stale_device_memory(cuda_ok, name):
     assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref)
 
 
-@pytest.mark.parametrize("name,groups", [("rand256_s0", 2), ("rand256_s0", 3), ("sph64j", 2)])
+@pytest.mark.parametrize("name,groups", [("sph64j", 2), ("sph64j", 4)])
 def test_virtual_groups_reproduce_multi_cluster_bitwise(cuda_ok, name, groups, monkeypatch):
-    """The pair-sharded exchange (participants in per-group buffers, fixed participant order)
-    run as `groups` virtual groups on one GPU must equal the single-group multi-cluster solve."""
+    """n <= 64 (multi-cluster kernel): the pair-sharded exchange (participants in per-group
+    buffers, fixed participant order) run as `groups` virtual groups on one GPU must equal the
+    single-group multi-cluster solve bit for bit."""
     from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve
     spec, cfg, ref = load_golden(name)
     base = am_solve(spec, SolverConfig(max_iters=40), cache=FactorCache())
@@ -185,6 +186,37 @@ def test_virtual_groups_reproduce_multi_cluster_bitwise(cuda_ok, name, groups, m
     assert rep.iterations == base.iterations
     np.testing.assert_array_equal(rep.coefficients, base.coefficients)
     np.testing.assert_array_equal(rep.residual_max_history, base.residual_max_history)
+
+
+@pytest.mark.parametrize("name,groups", [("rand256_s0", 2), ("rand256_s0", 3), ("rand256_s0", 8),
+                                         ("rand128_s0", 4)])
+def test_pair_sharded_groups_match_reference(cuda_ok, name, groups, monkeypatch):
+    """n > 64 (large-fleet kernel): G pair-sharded groups -- each a contiguous range of agent
+    pairs, its own partial right-hand sides exchanged once per iteration and summed in rank
+    order -- emulated as G groups of CTAs in one launch on this GPU (ranks that wait on one
+    another must share a launch on one device).  The full solve must meet the reference bar
+    (a different summation order than G = 1, so not bitwise) with the same iterations."""
+    from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve
+    spec, cfg, ref = load_golden(name)
+    monkeypatch.setenv("SWARM_VIRTUAL_GROUPS", str(groups))
+    rep = am_solve(spec, SolverConfig(**cfg), cache=FactorCache())
+    assert rep.iterations == int(ref["iterations"])
+    assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref)
+    np.testing.assert_allclose(rep.residual_max_history, ref["residual_max_history"], rtol=1e-7)
+    rep2 = am_solve(spec, SolverConfig(**cfg), cache=FactorCache())
+    np.testing.assert_array_equal(rep2.coefficients, rep.coefficients)  # deterministic per G
+
+
+def test_large_fleet_kernel_on_small_fleets_matches_reference(cuda_ok, monkeypatch):
+    """SWARM_LARGE=2 routes any fleet through the large-fleet kernel: partial agent blocks,
+    a single block, odd agent counts."""
+    from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve
+    monkeypatch.setenv("SWARM_LARGE", "2")
+    for name in ("rand48_s0", "rand20_s0", "rand3_s0", "rand5_s1", "sph64j", "circ16j"):
+        spec, cfg, ref = load_golden(name)
+        rep = am_solve(spec, SolverConfig(**cfg), cache=FactorCache())
+        assert rep.iterations == int(ref["iterations"]), name
+        assert rel_err(rep.coefficients, ref["coefficients"]) <= coeff_tol(ref), name
 
 
 @pytest.mark.parametrize("name", ["rand128_s0", "circ16j"])
