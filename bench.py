@@ -17,13 +17,18 @@ whole batch (every scenario to convergence or max_iters) in one device launch.
   (profiles/ubench_r1.txt: 64 lanes/clk/SM x 148 SMs x SM clock x 2).
 * ``cpu_baseline``: the reference algorithm (oracle/am_oracle.py, numpy/scipy LU path,
   warm factors) on a bounded sample, one process per host core.
+* ``fp32``: the same batch in the optional FP32 mode, device time.
+* ``single_solve_ms``: BASELINE's "ms per joint solve at 16/32/64/256 agents" -- circ16j,
+  rand32_s0, sph64j, rand128_s0, rand256_s0: device loop (best of 3), whole am_solve call,
+  FP32 mode, the same-run CPU reference (oracle port, 1 thread; a bounded prefix for
+  n > 64) and the loop's roofline fraction.
 * Multi-GPU (torchrun): scenarios are independent units, so ranks shard them with no
   data-path collective (NCCL only for the barrier and the max-over-ranks timing).
-  Default ``--scaling weak``: every rank solves its own batch of ``--batch`` scenarios
-  (rank r: seeds r*batch .. (r+1)*batch-1), value = all scenarios / max-over-ranks time.
-  ``--scaling strong``: the one batch of ``--batch`` (seeds 0..batch-1) split 1/N per rank
-  (BASELINE config 4 read literally; at N=8 each GPU gets 128 scenarios for 74 clusters,
-  so two cluster rounds bound it at ~6.6x).
+  Default ``--scaling strong`` (BASELINE config 4 read literally): the one batch of
+  ``--batch`` (seeds 0..batch-1) split 1/N per rank; at N=8 each GPU gets 128 scenarios for
+  74 two-CTA clusters (two cluster rounds: ~84% of the per-GPU rate at 1024).
+  ``--scaling weak``: every rank solves its own batch of ``--batch`` scenarios (rank r:
+  seeds r*batch .. (r+1)*batch-1), value = all scenarios / max-over-ranks time.
 
 ``--impl reference`` times the reference algorithm on the host cores instead.
 """
@@ -57,12 +62,19 @@ def scenarios(lo: int, hi: int):
 # CPU reference (oracle port of the reference algorithm), one process per core
 
 
+def sample_seeds(count: int) -> list[int]:
+    """A spread subset of the bench population (seeds 0..BATCH-1), for the bounded CPU samples."""
+    count = max(1, min(count, BATCH))
+    return sorted({(i * BATCH) // count + (BATCH // count) // 2 for i in range(count)})
+
+
 def _cpu_worker(seeds):
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from scipy.linalg import lu_factor
 
     from oracle import am_oracle
-    specs = scenarios(seeds[0], seeds[1])
+    from paper_2011_04240_b200 import generate_random
+    specs = [generate_random(32, (8.0, 8.0, 3.0), 0.4, s) for s in seeds]
     pr = am_oracle.Problem(specs[0])
     rhos, _ = am_oracle.schedule()
     factors = [lu_factor(pr.kkt(r), check_finite=False) for r in rhos]  # warm cache (reference excludes it)
@@ -76,7 +88,9 @@ def _cpu_worker(seeds):
 def cpu_reference(n_per_core: int, cores: int | None = None):
     import multiprocessing as mp
     cores = cores or os.cpu_count() or 1
-    jobs = [(1024 + i * n_per_core, 1024 + (i + 1) * n_per_core) for i in range(cores)]
+    seeds = sample_seeds(n_per_core * cores)
+    jobs = [seeds[i::cores] for i in range(cores) if seeds[i::cores]]
+    cores = len(jobs)
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
@@ -171,7 +185,8 @@ def run_reference(args):
     for _ in range(args.steps):
         vals.append(cpu_reference(per_core, cores))
     v = sum(r["solves_per_s"] for r in vals) / len(vals)
-    sample = f"{per_core * cores} rand32 scenarios (seeds 1024..) per step, warm LU factors, 1 process/core"
+    sample = (f"{per_core * cores} rand32 scenarios per step, a spread subset of the bench's seeds 0..{BATCH - 1}, "
+              "warm LU factors, 1 process/core")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": 1e3 * vals[-1]["wall_s"],
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
@@ -182,20 +197,92 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def single_solve_ms(names=("circ16j", "rand32_s0", "sph64j", "rand256_s0")):
+FLOP_PER_PAIR_SAMPLE_F = FLOP_PER_PAIR_SAMPLE
+
+
+def _cpu_single(name: str, max_iters: int | None = None):
+    """Same-run CPU time of the reference algorithm (oracle port, numpy/scipy LU, 1 thread, warm
+    factors): best of 3 for full solves, or the mean per-iteration time of a bounded prefix."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from scipy.linalg import lu_factor
+
+    from oracle import am_oracle
+    from paper_2011_04240_b200 import named
+    spec = named(name)
+    pr = am_oracle.Problem(spec)
+    rhos, _ = am_oracle.schedule()
+    if max_iters is None:
+        factors = [lu_factor(pr.kkt(r), check_finite=False) for r in rhos]
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            out = am_oracle.solve(spec, factors=factors)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return {"loop_ms": round(best * 1e3, 3), "iterations": out["iterations"], "threads": 1,
+                "per_iteration_ms": round(best * 1e3 / out["iterations"], 4)}
+    f0 = lu_factor(pr.kkt(rhos[0]), check_finite=False)  # only stage 0 runs in a short prefix
+    t0 = time.perf_counter()
+    out = am_oracle.solve(spec, max_iters=max_iters, factors=[f0] * len(rhos))
+    per = (time.perf_counter() - t0) / out["iterations"]
+    return {"per_iteration_ms": round(per * 1e3, 3), "iterations_timed": out["iterations"], "threads": 1,
+            "note": f"bounded sample: first {max_iters} iterations (stage 0), initialization included"}
+
+
+def _pair_samples(spec, iters: int) -> float:
+    n, m = len(spec.start), spec.num_samples
+    return float((n * (n - 1) // 2 + n * len(spec.obstacles)) * m * (iters + 1))
+
+
+def single_solve_ms(names=("circ16j", "rand32_s0", "sph64j", "rand128_s0", "rand256_s0"), cpu=True,
+                    fp64_peak=37.2, hbm_peak=6447.8):
+    """BASELINE metric "ms per joint solve at 16/32/64/256 agents": device loop (best of 3),
+    whole am_solve call, FP32 mode, the same-run CPU reference, and the roofline fraction of
+    the loop (FP64 pipe for the cluster kernel, HBM for the large-fleet kernel's streamed
+    multipliers)."""
     from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve, named
     cache = FactorCache()
     out = {}
     for nm in names:
         spec = named(nm)
-        am_solve(spec, SolverConfig(), cache=cache)
-        best = None
-        for _ in range(3):
-            r = am_solve(spec, SolverConfig(), cache=cache)
-            t = r.timings["loop_s"] * 1e3
-            best = t if best is None else min(best, t)
-        out[nm] = {"ms": round(best, 4), "iterations": r.iterations, "converged": r.converged,
-                   "end_to_end_ms": round(r.timings["total_s"] * 1e3, 3)}
+        row = {}
+        for fp32 in (False, True):
+            am_solve(spec, SolverConfig(fp32=fp32), cache=cache)
+            best, r = None, None
+            for _ in range(3):
+                r = am_solve(spec, SolverConfig(fp32=fp32), cache=cache)
+                t = r.timings["loop_s"] * 1e3
+                best = t if best is None else min(best, t)
+            if not fp32:
+                n = len(spec.start)
+                ps = _pair_samples(spec, r.iterations)
+                large = n > 64
+                bytes_ = BYTES_PER_PAIR_SAMPLE * ps
+                flops = FLOP_PER_PAIR_SAMPLE * ps
+                row.update({"ms": round(best, 4), "iterations": r.iterations, "converged": r.converged,
+                            "end_to_end_ms": round(r.timings["total_s"] * 1e3, 3),
+                            "kernel": "am_large_kernel" if large else "am_cluster_kernel"})
+                if large:
+                    gbs = bytes_ / (best / 1e3) / 1e9
+                    row["roofline"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                                       "frac": round(gbs / hbm_peak, 4),
+                                       "per_unit": "48 B multipliers (read+write) per pair-sample per iteration"}
+                else:
+                    tf = flops / (best / 1e3) / 1e12
+                    row["roofline"] = {"bound": "fp64", "achieved": round(tf, 3), "peak": fp64_peak,
+                                       "unit": "TFLOP/s", "frac": round(tf / fp64_peak, 4),
+                                       "per_unit": "85 FLOP per pair-sample per iteration"}
+            else:
+                row["fp32_ms"] = round(best, 4)
+                row["fp32_iterations"] = r.iterations
+        if cpu:
+            ref = _cpu_single(nm, max_iters=None if len(spec.start) <= 64 else 3)
+            row["cpu"] = ref
+            if "loop_ms" in ref:
+                row["speedup_vs_cpu"] = round(ref["loop_ms"] / row["ms"], 1)
+            else:
+                row["speedup_vs_cpu_per_iteration"] = round(ref["per_iteration_ms"] / (row["ms"] / row["iterations"]), 1)
+        out[nm] = row
     return out
 
 
@@ -206,12 +293,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--cpu-per-core", type=int, default=2, help="cpu_baseline sample: scenarios per core")
     ap.add_argument("--ref-per-core", type=int, default=1)
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-single", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -282,6 +370,43 @@ def main():
     dev_ms_max = allreduce_max(dev_ms, world, dev)
     step_ms = dev_ms_max / args.steps
     value = total / (step_ms / 1e3)
+
+    # the optional FP32 mode (SolverConfig(fp32=True)) on the same device-resident batch
+    fp32 = None
+    if not args.no_fp32:
+        d_it32 = torch.empty_like(d_it)
+
+        def launch32():
+            plan.solve_device(B, d_c0.data_ptr(), d_beq.data_ptr(), d_geom.data_ptr(), sched.switch_every,
+                              cfg.max_iters, cfg.tolerance, d_cout.data_ptr(), d_hist.data_ptr(), d_it32.data_ptr(),
+                              d_cv.data_ptr(), stream=stream.cuda_stream, fp32=True)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                launch32()
+        torch.cuda.synchronize(dev)
+        ev32 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.zero_()
+                ev32[i][0].record(stream)
+                launch32()
+                ev32[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        ms32 = allreduce_max(sum(a.elapsed_time(b) for a, b in ev32), world, dev) / args.steps
+        it32 = d_it32.cpu().numpy()
+        fp32 = {"value": round(total / (ms32 / 1e3), 2), "unit": "solves/s", "ms_per_step": round(ms32, 4),
+                "iterations_mean": round(float(it32.mean()), 2),
+                "iterations_equal_fp64_frac": round(float((it32 == iters).mean()), 4),
+                "speedup_vs_fp64": round(step_ms / ms32, 3),
+                "mode": "FP32 pair state (multipliers + pair arithmetic), FP64 positions/sums/solve; "
+                        "tolerances in DESIGN.md §8"}
+        # leave the FP64 outputs in place for the checks below
+        with torch.cuda.stream(stream):
+            launch()
+        torch.cuda.synchronize(dev)
 
     # end to end through the C ABI with page-locked host buffers (H2D of the inputs + loop +
     # D2H of the results inside the timed region, every step)
@@ -354,9 +479,12 @@ def main():
                                  f"({pair_samples:.3e} pair-samples per launch incl. init pass)",
                      "peak_source": "measured DFMA 64 lanes/clk/SM x 148 SMs x 1.965 GHz x 2 "
                                     "(profiles/ubench_r1.txt)"},
-        "roofline_hbm": {"bound": "hbm", "achieved": round(ach_bytes, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(ach_bytes / hbm_peak, 4),
-                         "per_unit": "48 B (lambda read+write) per pair-sample per iteration"},
+        "lambda_stream": {"achieved_gbs": round(ach_bytes, 1),
+                          "per_unit": "48 B (lambda read+write) per pair-sample per iteration",
+                          "note": "algorithmic multiplier traffic; the per-cluster slabs are L2-resident "
+                                  "(persisting window, DRAM sees a small fraction -- ncu traffic), so this is "
+                                  "an L2 rate, not an HBM fraction"},
+        "fp32": fp32,
         "clocks": sm_mhz,
         "precompute_s": round(precompute_s, 4),
         "iterations_mean": round(float(iters.mean()), 2),
@@ -364,14 +492,16 @@ def main():
         "e2e_matches_device_iters": ok,
     }
     if not args.no_single and world == 1:
-        line["single_solve_ms"] = single_solve_ms()
+        line["single_solve_ms"] = single_solve_ms(cpu=not args.no_cpu, fp64_peak=round(fp64_peak_tflops, 2),
+                                                  hbm_peak=hbm_peak)
     if not args.no_cpu and world == 1:
         cores = os.cpu_count() or 1
         ref = cpu_reference(args.cpu_per_core, cores)
-        line["cpu_baseline"] = {"value": round(ref["solves_per_s"], 3), "unit": "solves/s", "cores": cores,
+        line["cpu_baseline"] = {"value": round(ref["solves_per_s"], 3), "unit": "solves/s", "cores": ref["cores"],
                                 "kind": "port",
-                                "sample": f"{ref['solves']} rand32 scenarios (seeds 1024..), oracle/am_oracle.py "
-                                          f"(reference LU algorithm, numpy/scipy), warm factors, 1 process/core"}
+                                "sample": f"{ref['solves']} rand32 scenarios, a spread subset of the bench's seeds "
+                                          f"0..{BATCH - 1}, oracle/am_oracle.py (reference LU algorithm, "
+                                          f"numpy/scipy), warm factors, 1 process/core"}
     print(json.dumps(line), flush=True)
 
 

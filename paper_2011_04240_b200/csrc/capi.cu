@@ -351,6 +351,32 @@ cudaEvent_t multi_event(int device) {
   return evs[device];
 }
 
+// The device-wide L2 set-aside for persisting lines: the batch kernel's multiplier slabs and
+// the FP32 large-fleet multipliers want it; a kernel that streams through L2 (FP64 large
+// fleets) loses ~40% with it in place (profiles/large_l2_setaside_r2.txt), so every launch sets
+// what it needs (device-wide, sticky: tracked per device to skip redundant calls).
+std::mutex g_persist_mu;
+int g_persist_state[64];
+bool g_persist_init = false;
+size_t set_persisting_l2(int device, bool on) {
+  std::lock_guard<std::mutex> lk(g_persist_mu);
+  if (!g_persist_init) {
+    for (auto& v : g_persist_state) v = -1;
+    g_persist_init = true;
+  }
+  int max_persist = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+  if (device < 0 || device >= 64 || max_persist <= 0) return 0;
+  const int want = on ? 1 : 0;
+  if (g_persist_state[device] != want) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, on ? (size_t)max_persist : 0);
+    if (!on) cudaCtxResetPersistingL2Cache();
+    cudaGetLastError();
+    g_persist_state[device] = want;
+  }
+  return on ? (size_t)max_persist : 0;
+}
+
 struct ShardExt {
   int G, rank;
   void* bufs[8];
@@ -574,12 +600,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, pl->device);
     cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, pl->device);
     if ((!pe || std::atoi(pe) != 0) && max_persist > 0 && max_window > 0) {
-      if (!pl->persist_set) {
-        // device-wide carve-out for persisting lines (set once per plan's device)
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-        cudaGetLastError();
-        pl->persist_set = 1;
-      }
+      set_persisting_l2(pl->device, true);
       const size_t used = (size_t)L.nclusters * L.C * L.lam_per_cta * esize;
       const int TPWl = 32 / L.W, NWl = L.NT / 32;
       const long long rows_w = ceil_div((long long)ceil_div(L.tmax, TPWl) * L.nsteps, NWl);
@@ -739,6 +760,9 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
   if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 8192 * sizeof(long long)));
   if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 8192 * sizeof(long long), s));
   k.tstamp = timers ? d_ts : nullptr;
+  // FP64: no persisting set-aside (the multipliers stream through L2 evict-first and the unit
+  // slots / positions need the whole cache); FP32: the multipliers fit and persist
+  if (!f32 || std::getenv("SWARM_NO_L2_PERSIST")) set_persisting_l2(pl->device, false);
   // grid-barrier kernels are serialized device-wide (see run())
   std::unique_lock<std::mutex> multi_lock(g_multi_mu);
   cudaEvent_t multi_ev = multi_event(pl->device);
@@ -757,11 +781,7 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, pl->device);
     cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, pl->device);
     if (max_persist > 0 && max_window > 0) {
-      if (!pl->persist_set) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
-        cudaGetLastError();
-        pl->persist_set = 1;
-      }
+      set_persisting_l2(pl->device, true);
       const size_t used = off.back() * esize;
       at[na].id = cudaLaunchAttributeAccessPolicyWindow;
       at[na].val.accessPolicyWindow.base_ptr = pl->d_lam;
