@@ -56,12 +56,14 @@ struct LgParams {
   const int* cta_first;            // G x (cpg + 1): CTA c of group g owns [cta_first[g(cpg+1)+c], ...+1])
   const long long* lam_off;        // element offset of unit u's multiplier rows, index u - u_range[g_base]
   void* lam;                       // this launch's multipliers (double, or float in FP32 mode)
-  double* qbuf;                    // all units: [2 sides][3 axes][32 lanes] partial S'b rows
+  double* qbuf;                    // 2 pass parities x all units: [2 sides][3 axes][32 lanes] partial S'b rows
+  long long q_stride;              // doubles per parity of qbuf
   double* X;                       // per group: m x 3 x npad positions (stride x_stride)
   double* cbuf;                    // per group: 3 x n x NVMAX coefficients (stride c_stride)
   long long x_stride, c_stride;
-  double* cta_nrm;                 // per CTA of the launch: (sum r^2, max |r|) of the last P phase
-  unsigned long long* bnd;         // per group (stride 16): 2 iteration parities, boundary max bits
+  double* cta_nrm;                 // 2 pass parities x per CTA of the launch: (sum r^2, max |r|) of a P phase
+  unsigned long long* bnd;         // per group (stride 16): 3 rotating iterations, boundary max bits
+  unsigned* blk_ready;             // per group (stride LG_MAXB * 32): rows of each agent block published
   unsigned* gbar;                  // per group (stride 32): grid barrier {count, generation}
   double* xch[8];                  // per group g: 2 parities x (3 n NVMAX + 4) exchange doubles
   unsigned* sysbar;                // barrier over every group's CTAs (G > 1)
@@ -86,7 +88,8 @@ struct LgCtx {
   double* cbuf;
   unsigned long long* bnd;
   unsigned* gbar;
-  const double* nrm;  // the group's CTA norm slots
+  unsigned* rdy;      // the group's block-ready counters (stride 32)
+  const double* nrm;  // the group's CTA norm slots (parity 0; parity 1 at + 2 * G * cpg)
 };
 
 __device__ __forceinline__ LgCtx lg_ctx(const LgParams& p) {
@@ -103,6 +106,7 @@ __device__ __forceinline__ LgCtx lg_ctx(const LgParams& p) {
   c.bnd = p.bnd + c.vg * 16;
   c.gbar = p.gbar + c.vg * 32;
   c.nrm = p.cta_nrm + 2LL * c.vg * p.cpg;
+  c.rdy = p.blk_ready + c.vg * LG_MAXB * 32;
   c.lxy = __ldg(p.geom);
   c.lz = __ldg(p.geom + 1);
   return c;
@@ -125,7 +129,7 @@ __host__ __device__ inline LgSmem lg_smem(int m, int chunk_rows) {
   s.mat = take(StageMats<NVMAX>::SIZE * 8);
   s.blist = take(LG_MAXB * LG_MAXB * 4 + (LG_MAXB * (LG_MAXB + 1) / 2 + 1) * 4);
   s.bbar = take(18 * 8);
-  s.misc = take(8 * 8);
+  s.misc = take(8 * 8 + LG_MAXB * 4);  // broadcast words + per-block seen epochs
   s.total = o;
   return s;
 }
@@ -339,9 +343,34 @@ __device__ __forceinline__ void lg_steps(int s_lo, int s_hi, int row0, int a, in
 }
 
 // P phase of one CTA: its units, NW warps, multipliers streamed per warp.
+// Wait until agent block b's rows of epoch `epoch` are published (positions X of the last R
+// phase): lane 0 polls the block's counter (acquire) once per block and epoch per CTA.
+__device__ __forceinline__ void lg_wait_block(const LgParams& p, const LgCtx& cx, int* seen, int b, int epoch) {
+  if (((volatile int*)seen)[b] >= epoch) return;
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    const unsigned nb = (unsigned)min(32, p.n - 32 * b);
+    const unsigned target = 3u * nb * (unsigned)epoch;
+    const unsigned* c = cx.rdy + b * 32;
+    unsigned v;
+    unsigned long long t0 = 0, t;
+    for (unsigned it = 0;; ++it) {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      if (v >= target) break;
+      if ((it & 1023u) == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (it == 0) t0 = t;
+        else if (t - t0 > 30000000000ull) __trap();
+      }
+    }
+    ((volatile int*)seen)[b] = epoch;
+  }
+  __syncwarp();
+}
+
 template <int NVMAX, bool INIT, bool SPHERE, bool F32>
 __device__ __forceinline__ void lg_pair_phase(const LgParams& p, const LgCtx& cx, unsigned char* smb, const LgSmem& L,
-                                              bool lam_zero, const StepConst& sc, unsigned& par_bits) {
+                                              bool lam_zero, const StepConst& sc, unsigned& par_bits, int pass) {
   using R = typename std::conditional<F32, float, double>::type;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int CH = lg_chunk_rows(F32);
@@ -387,7 +416,12 @@ __device__ __forceinline__ void lg_pair_phase(const LgParams& p, const LgCtx& cx
     const int nA = min(32, p.n - 32 * A), nB = min(32, p.n - 32 * B);
     const long long uoff = p.lam_off[u - ubase];
     const int nrow = (int)(p.lam_off[u - ubase + 1] - uoff) / 96;
-    if (nrow == 0) continue;  // the empty second half of a diagonal unit
+    if (nrow == 0) continue;  // a diagonal block of one agent
+    // positions of this pass: published by the R phase (epoch = pass + 1: the initial positions
+    // are epoch 1)
+    int* seen = reinterpret_cast<int*>(smb + L.misc) + 8;
+    lg_wait_block(p, cx, seen, A, pass + 1);
+    if (!diag) lg_wait_block(p, cx, seen, B, pass + 1);
     const double* Xt = cx.X + (long long)t * 3 * p.npad;
     double xo[3];
 #pragma unroll
@@ -419,7 +453,7 @@ __device__ __forceinline__ void lg_pair_phase(const LgParams& p, const LgCtx& cx
         st.release(lane);
       }
     }
-    double* q = p.qbuf + (long long)u * 192;
+    double* q = p.qbuf + (pass & 1) * p.q_stride + (long long)u * 192;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
       q[ax * 32 + lane] = lane < nA ? acc[ax] : 0.0;
@@ -438,8 +472,9 @@ __device__ __forceinline__ void lg_pair_phase(const LgParams& p, const LgCtx& cx
       double a2 = lane < LG_NW ? wslot[2 * lane] : 0.0, am = lane < LG_NW ? wslot[2 * lane + 1] : 0.0;
       warp_sum_max(a2, am);
       if (lane == 0) {
-        p.cta_nrm[2 * blockIdx.x] = a2;
-        p.cta_nrm[2 * blockIdx.x + 1] = am;
+        double* slot = p.cta_nrm + (pass & 1) * 2LL * p.vgroups * p.cpg + 2 * blockIdx.x;
+        slot[0] = a2;
+        slot[1] = am;
       }
     }
   }
@@ -493,7 +528,7 @@ __device__ __forceinline__ void lg_solve_row(const LgParams& p, const LgCtx& cx,
       bmx = fabs(v - __ldg(bj + lane));
     }
     bmx = warp_max(bmx);
-    if (lane == 0 && bmx > 0.0) atomicMax(cx.bnd + (k & 1), (unsigned long long)__double_as_longlong(bmx));
+    if (lane == 0 && bmx > 0.0) atomicMax(cx.bnd + (k % 3), (unsigned long long)__double_as_longlong(bmx));
   }
   if (lane < NVMAX) {
     double v = 0.0;
@@ -538,7 +573,7 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
       const int r = r_lo + rl;
       const int ax = r / n, j = r - ax * n;
       const int b = j >> 5, l = j & 31;
-      const double* qb = p.qbuf + ax * 32 + l;
+      const double* qb = p.qbuf + (k & 1) * p.q_stride + ax * 32 + l;  // written by pass k
       double v[2 * LG_MAXB];
 #pragma unroll
       for (int e = 0; e < LG_MAXB; ++e) {
@@ -605,7 +640,18 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
   if (mode == 1 || mode == 2) {
     // qs (generic-proxy writes/reads) lives in the ring the next P phase fills by TMA (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
+  }
+  __syncthreads();
+  if (mode != 2 && threadIdx.x == 0 && nr > 0) {
+    // publish: this CTA's rows of each agent block are in X (release after the CTA barrier)
+    int cnt[LG_MAXB];
+#pragma unroll
+    for (int b = 0; b < LG_MAXB; ++b) cnt[b] = 0;
+    for (int r = r_lo; r < r_hi; ++r) cnt[(r % n) >> 5]++;
+    __threadfence();
+#pragma unroll
+    for (int b = 0; b < LG_MAXB; ++b)
+      if (cnt[b]) atomicAdd(cx.rdy + b * 32, (unsigned)cnt[b]);
   }
 }
 
@@ -662,11 +708,12 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
   long long* ts = (p.tstamp && blockIdx.x == 0 && p.g_base == 0 && threadIdx.x == 0) ? p.tstamp : nullptr;
 
   // initialization: positions of the straight lines, then the INIT pair pass (solver.py:309-352)
+  if (threadIdx.x < LG_MAXB) reinterpret_cast<int*>(smb + L.misc)[8 + threadIdx.x] = 0;  // seen epochs
+  __syncthreads();
   lg_rows<NVMAX>(p, cx, smb, L, 0, 0);
-  grid_barrier(cx.gbar, p.cpg, false);
-  if (sphere) lg_pair_phase<NVMAX, true, true, F32>(p, cx, smb, L, true, sc, par_bits);
-  else lg_pair_phase<NVMAX, true, false, F32>(p, cx, smb, L, true, sc, par_bits);
-  if (cx.cta == 0 && threadIdx.x == 0) { cx.bnd[0] = 0ull; cx.bnd[1] = 0ull; }
+  if (sphere) lg_pair_phase<NVMAX, true, true, F32>(p, cx, smb, L, true, sc, par_bits, 0);
+  else lg_pair_phase<NVMAX, true, false, F32>(p, cx, smb, L, true, sc, par_bits, 0);
+  if (cx.cta == 0 && threadIdx.x == 0) { cx.bnd[0] = 0ull; cx.bnd[1] = 0ull; cx.bnd[2] = 0ull; }
   grid_barrier(cx.gbar, p.cpg, false);
 
   int prev_stage = -1, iters = 0, conv = 0;
@@ -683,7 +730,7 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
     }
     // residual norms of the previous pass: the group's CTAs in fixed order (every CTA alike)
     double s2 = 0.0, mx = 0.0;
-    if (k > 0 && threadIdx.x < 32) lg_norms(cx.nrm, p.cpg, s2, mx);
+    if (k > 0 && threadIdx.x < 32) lg_norms(cx.nrm + (k & 1) * 2LL * p.vgroups * p.cpg, p.cpg, s2, mx);
     __syncthreads();  // the stage matrices are in place
     if (p.G > 1) {
       // this group's R rows -> its exchange buffer, norm totals alongside; meet every group
@@ -712,7 +759,7 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
     stamp(tsr, 1);
     if (k > 0) {
       // convergence test on iteration k-1 (solver.py:444-457), identical in every CTA / group
-      const double bm = __longlong_as_double((long long)__ldcg(cx.bnd + ((k - 1) & 1)));
+      const double bm = __longlong_as_double((long long)__ldcg(cx.bnd + ((k - 1) % 3)));
       if (cx.cta == 0 && cx.g == 0 && threadIdx.x == 0) {
         p.hist[k - 1] = sqrt(s2);
         p.hist[p.max_iters + k - 1] = mx;
@@ -730,13 +777,14 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
     sc.inv_rho = mat[SM::RHO + 1];
     sc.inv_rho_next = p.inv_rho[stage_n];
     stamp(tsr, 2);
-    grid_barrier(cx.gbar, p.cpg, false);
+    // no grid barrier here: every unit waits for the published rows of its two agent blocks
     stamp(tsr, 3);
     long long tp0 = 0;
     if (p.tstamp && k == 50 && threadIdx.x == 0) tp0 = clock64();
-    if (cx.cta == 0 && threadIdx.x == 0) cx.bnd[(k + 1) & 1] = 0ull;  // written by the R phase of k+1
-    if (sphere) lg_pair_phase<NVMAX, false, true, F32>(p, cx, smb, L, k == 0, sc, par_bits);
-    else lg_pair_phase<NVMAX, false, false, F32>(p, cx, smb, L, k == 0, sc, par_bits);
+    // bnd slot of iteration k+1 (last read by the test of iteration k-1, before the last barrier)
+    if (cx.cta == 0 && threadIdx.x == 0) cx.bnd[(k + 1) % 3] = 0ull;
+    if (sphere) lg_pair_phase<NVMAX, false, true, F32>(p, cx, smb, L, k == 0, sc, par_bits, k + 1);
+    else lg_pair_phase<NVMAX, false, false, F32>(p, cx, smb, L, k == 0, sc, par_bits, k + 1);
     stamp(tsr, 4);
     if (p.tstamp && k == 50 && threadIdx.x == 0) p.tstamp[4096 + blockIdx.x] = clock64() - tp0;  // per-CTA P phase
     grid_barrier(cx.gbar, p.cpg, false);

@@ -695,8 +695,10 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
   const size_t n_ab = Lg.ab.size(), n_af = Lg.ab_first.size(), n_ur = Lg.u_range.size(), n_cf = Lg.cta_first.size();
   const size_t tab_bytes = ((n_ab + n_af + n_ur + n_cf) * 4 + 15) / 16 * 16 + off.size() * 8;
   const long long xst = 3LL * n * NV + 4;
-  const size_t q_bytes = (size_t)Lg.U * 192 * 8, x_bytes = (size_t)m * 3 * Lg.npad * 8, cb_bytes = 3ULL * n * NV * 8;
-  const size_t nrm_bytes = (size_t)grid * 16, bnd_bytes = (size_t)vgroups * 16 * 8, bar_bytes = (size_t)(vgroups + 1) * 128;
+  const size_t q_bytes = 2 * (size_t)Lg.U * 192 * 8, x_bytes = (size_t)m * 3 * Lg.npad * 8, cb_bytes = 3ULL * n * NV * 8;
+  const size_t nrm_bytes = 2 * (size_t)grid * 16, bnd_bytes = (size_t)vgroups * 16 * 8;
+  // barrier words (one 128-byte line per group + the system barrier), then the block-ready counters
+  const size_t bar_bytes = (size_t)(vgroups + 1) * 128 + (size_t)vgroups * swarm::LG_MAXB * 128;
   const size_t xch_bytes = (ext || G == 1) ? 0 : (size_t)G * 2 * xst * 8;
   size_t o = 0;
   auto carve = [&](size_t bytes) { const size_t r = o; o += (bytes + 255) / 256 * 256; return r; };
@@ -735,6 +737,8 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
   k.G = G; k.g_base = g_base; k.vgroups = vgroups; k.cpg = cpg;
   k.lam = pl->d_lam;
   k.qbuf = reinterpret_cast<double*>(base + o_q);
+  k.q_stride = (long long)Lg.U * 192;
+  k.blk_ready = reinterpret_cast<unsigned*>(base + o_bar + (size_t)(vgroups + 1) * 128);
   k.X = reinterpret_cast<double*>(base + o_x);
   k.cbuf = reinterpret_cast<double*>(base + o_cb);
   k.x_stride = (long long)(x_bytes / 8);
@@ -808,7 +812,7 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
         std::fprintf(stderr, " %d:%lld(u%d-%d)", c, h[4096 + c], Lg.cta_first[c], Lg.cta_first[c + 1]);
       std::fprintf(stderr, "\n");
     }
-    static const char* names[] = {"norms+exchange", "solve+positions", "barrier2", "pairs", "barrier1"};
+    static const char* names[] = {"norms+exchange", "solve+positions", "-", "pairs", "barrier"};
     double acc[5] = {0};
     int cnt = 0;
     for (int it = 1; it < 255 && h[16 * (it + 1)]; ++it, ++cnt) {
