@@ -231,6 +231,11 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       return ceil_div(pl->m, K * C);
     };
     std::stable_sort(cands.begin(), cands.end(), [&](int a, int b) { return per_cta(a) < per_cta(b); });
+  } else if (batch == 1 && pl->n <= 8) {
+    // latency, tiny fleets: 8-CTA clusters match 16 per iteration (rand5 7.8 vs 8.1 us, rand8
+    // 8.3 vs 8.2, profiles/small_cluster_sweep_r2.txt) with half the exchange/barrier partners,
+    // and their per-iteration cost follows the obstacle count (acceptance C8)
+    cands = {8, 16, 4, 2, 1};
   } else if (batch == 1) {
     cands = {16, 8, 4, 2, 1};  // latency: spread one scenario widest
   } else {

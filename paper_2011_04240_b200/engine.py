@@ -18,17 +18,19 @@ launch (the reference runs those through a thread pool, bench.py:120-158).
 
 from __future__ import annotations
 
+import itertools
 import logging
 import math
 import sys
 import time
 import weakref
 from dataclasses import dataclass, field
+from operator import attrgetter
 
 import numpy as np
 
 from . import kkt, metrics, native, poly
-from .spec import obstacle_axes, validate
+from .spec import obstacle_axes, validate, validate_batch
 
 log = logging.getLogger(__name__)
 
@@ -250,7 +252,21 @@ def default_cache() -> kkt.FactorCache:
 # --- host-side packing ---------------------------------------------------------------------
 
 
-def pack(specs, basis: poly.Basis):
+def boundary_arrays(specs) -> np.ndarray:
+    """(B, 2, 3, n, 3) boundary states: scenario, start/goal, pos/vel/acc, agent, axis.
+
+    One C-level pass over the state objects (attribute getters feeding ``np.fromiter``):
+    the batch entry touches no per-agent Python beyond it."""
+    B, n = len(specs), len(specs[0].start)
+    get = attrgetter("position", "velocity", "acceleration")
+    chain = itertools.chain.from_iterable
+    states = [st for spec in specs for side in (spec.start, spec.goal) for st in side]
+    flat = np.fromiter(chain(chain(map(get, states))), dtype=float, count=len(states) * 9)
+    # flat order: scenario, start/goal, agent, pos/vel/acc, axis
+    return flat.reshape(B, 2, n, 3, 3).transpose(0, 1, 3, 2, 4)
+
+
+def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None):
     """Scenario batch -> (c0 (B,3,n,nv), b_eq (B,3,n,6), geom (B, 2+5 n_obs)).
 
     b_eq rows per agent and axis: [pos0, vel0, acc0, posT, velT, accT]
@@ -259,22 +275,18 @@ def pack(specs, basis: poly.Basis):
     B = len(specs)
     n = len(specs[0].start)
     n_obs = len(specs[0].obstacles)
-    bnd = np.empty((B, 2, 3, n, 3))  # scenario, start/goal, pos/vel/acc, agent, axis
-    for b, spec in enumerate(specs):
-        for e, states in enumerate((spec.start, spec.goal)):
-            bnd[b, e, 0] = [s.position for s in states]
-            bnd[b, e, 1] = [s.velocity for s in states]
-            bnd[b, e, 2] = [s.acceleration for s in states]
+    if bnd is None:
+        bnd = boundary_arrays(specs)
     beq = np.ascontiguousarray(bnd.transpose(0, 4, 3, 1, 2).reshape(B, 3, n, 6))
     c0 = np.ascontiguousarray(poly.straight_line(basis, bnd[:, 0, 0].transpose(0, 2, 1),
                                                  bnd[:, 1, 0].transpose(0, 2, 1)))
     geom = np.empty((B, 2 + 5 * n_obs))
-    for b, spec in enumerate(specs):
-        geom[b, 0] = spec.geometry.l_xy
-        geom[b, 1] = spec.geometry.l_z
-        for k, obs in enumerate(spec.obstacles):
-            lxy, lz = obstacle_axes(spec, obs)
-            geom[b, 2 + 5 * k: 7 + 5 * k] = (*obs.center, lxy, lz)
+    geom[:, :2] = [(spec.geometry.l_xy, spec.geometry.l_z) for spec in specs]
+    if n_obs:
+        for b, spec in enumerate(specs):
+            for k, obs in enumerate(spec.obstacles):
+                lxy, lz = obstacle_axes(spec, obs)
+                geom[b, 2 + 5 * k: 7 + 5 * k] = (*obs.center, lxy, lz)
     return c0, beq, geom
 
 
@@ -409,42 +421,53 @@ def _descent_slack(spec, basis, plan, c0, beq, geom, schedule, config, iteration
 
 def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with_metrics=True,
                   foreign=None) -> list:
-    """Device outputs of one launch -> one SolveReport per scenario (reference field layout)."""
+    """Device outputs of one launch -> one SolveReport per scenario (reference field layout).
+
+    Whole-batch array work (trajectories, collision verdicts, arc length / smoothness) is done
+    once for all scenarios; single solves take the same path with B = 1, so batch and single
+    solves report identical trajectories and metrics."""
     t0, t1, t2, t3 = stamps
     h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
-    n, n_obs = len(specs[0].start), len(specs[0].obstacles)
-    reports = []
-    # trajectories exactly as the reference forms them (solver.py:133-136: c_axis @ P.T per axis),
-    # per scenario, so batch and single solves report identical trajectories and metrics
-    PT = basis.P.T
-    trajs = np.stack([np.stack([c[a] @ PT for a in range(3)], axis=-1) for c in out["c"]])
+    B = len(specs)
+    n = len(specs[0].start)
+    nv, m = basis.num_coeffs, basis.num_samples
+    # trajectories = c_axis @ P.T per axis (solver.py:133-136), all scenarios and axes in one product
+    c = out["c"]
+    trajs = np.ascontiguousarray((c.reshape(-1, nv) @ basis.P.T).reshape(B, 3, n, m).transpose(0, 2, 3, 1))
     tc0 = time.perf_counter()
-    cols = (metrics.collision_summary_device_batch(trajs, specs, _opt(config, "device", 0)) if with_metrics
-            else [None] * len(specs))
-    col_s = (time.perf_counter() - tc0) / len(specs)
+    if with_metrics:
+        cols = metrics.collision_summary_device_batch(trajs, specs, _opt(config, "device", 0))
+        arc, smooth = metrics.trajectory_metrics_batch_coeffs(c, basis.P)
+        arc_l, smooth_l = arc.tolist(), smooth.tolist()
+        arc_mean, smooth_mean = arc.mean(axis=1).tolist(), smooth.mean(axis=1).tolist()
+    metrics_s = (time.perf_counter() - tc0) / B
+    iters = out["iters"].tolist()
+    conv = out["converged"].tolist()
+    hist = out["hist"]
+    common = {"assembly_s": t1 - t0, "factorization_s": t2 - t1, "loop_s": loop_ms / 1e3, "h2d_s": h2d_ms / 1e3,
+              "d2h_s": d2h_ms / 1e3, "solve_call_s": t3 - t2, "metrics_s": metrics_s, "batch": B}
+    reports = []
     for b, spec in enumerate(specs):
-        it = int(out["iters"][b])
+        it = int(iters[b])
         before = cache.stats()
         cache.count_solve(3 * it)
         _sync_foreign(cache, foreign, before)
-        coeffs = out["c"][b]
-        traj = trajs[b]
-        tm0 = time.perf_counter()
-        rep_metrics = (metrics.final_metrics(spec, traj, device=_opt(config, "device", 0), collisions=cols[b])
-                       if with_metrics else {})
-        hist = out["hist"][b]
-        timings = {
-            "assembly_s": t1 - t0,
-            "factorization_s": t2 - t1,
-            "loop_s": loop_ms / 1e3,
-            "per_iteration_s": loop_ms / 1e3 / max(1, it),
-            "h2d_s": h2d_ms / 1e3,
-            "d2h_s": d2h_ms / 1e3,
-            "solve_call_s": t3 - t2,
-            "metrics_s": time.perf_counter() - tm0 + (col_s if cols[b] is not None else 0.0),
-            "total_s": time.perf_counter() - t0,
-            "batch": len(specs),
-        }
+        coeffs = c[b]
+        rep_metrics = {}
+        if with_metrics:
+            md, count = cols[b]
+            rep_metrics = {
+                "min_normalized_distance": None if math.isinf(md) else md,
+                "num_collision_violations": count,
+                "arc_length": arc_l[b],
+                "smoothness": smooth_l[b],
+                "mean_arc_length": arc_mean[b],
+                "mean_smoothness": smooth_mean[b],
+            }
+        h = hist[b, :, :it]
+        timings = dict(common)
+        timings["per_iteration_s"] = loop_ms / 1e3 / max(1, it)
+        timings["total_s"] = time.perf_counter() - t0
         diagnostics = {}
         if config.keep_state:
             _, lxy, lz, alpha, beta = _pair_state(spec, coeffs, basis)
@@ -455,18 +478,18 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
                 pair_vars=PairVariables(alpha=alpha, beta=beta, d=out["d"]),
                 multipliers=Multipliers(lambda_x=lam[0], lambda_y=lam[1], lambda_z=lam[2]),
                 rho=schedule.values[stage], stage=stage, iteration=it,
-                residual_norms=list(hist[0, :it]), residual_max=list(hist[1, :it]),
+                residual_norms=h[0].tolist(), residual_max=h[1].tolist(),
                 system=SystemView(spec, basis))
         reports.append(SolveReport(
-            trajectories=traj,
+            trajectories=trajs[b],
             coefficients=coeffs,
-            converged=bool(out["converged"][b]),
+            converged=bool(conv[b]),
             iterations=it,
-            residual_norm=float(hist[0, it - 1]) if it else 0.0,
-            residual_max_abs=float(hist[1, it - 1]) if it else 0.0,
-            residual_norm_history=[float(v) for v in hist[0, :it]],
-            residual_max_history=[float(v) for v in hist[1, :it]],
-            boundary_max_history=[float(v) for v in hist[2, :it]],
+            residual_norm=float(h[0, -1]) if it else 0.0,
+            residual_max_abs=float(h[1, -1]) if it else 0.0,
+            residual_norm_history=h[0].tolist(),
+            residual_max_history=h[1].tolist(),
+            boundary_max_history=h[2].tolist(),
             timings=timings,
             metrics=rep_metrics,
             cache_stats=(foreign if foreign is not None else cache).stats(),
@@ -484,19 +507,19 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
         return []
     if config.track_descent and len(specs) != 1:
         raise ValueError("track_descent is only available for single solves")
-    for spec in specs:
-        v = validate(spec)
+    _check_batch(specs)
+    t0 = time.perf_counter()
+    bnd = boundary_arrays(specs)
+    for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0]):
         if v:
             raise _infeasible(v)
-    _check_batch(specs)
     if config.keep_state and len(specs) != 1:
         raise ValueError("keep_state is only available for single solves")
-    t0 = time.perf_counter()
     spec0 = specs[0]
     n, n_obs = len(spec0.start), len(spec0.obstacles)
     basis = poly.for_spec(spec0)
     fp = kkt.fingerprint(basis, n, n_obs)
-    c0, beq, geom = pack(specs, basis)
+    c0, beq, geom = pack(specs, basis, bnd)
     t1 = time.perf_counter()
     cache, foreign = _resolve_cache(cache)
     schedule = config.schedule()

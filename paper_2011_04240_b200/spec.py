@@ -194,6 +194,55 @@ def validate(spec) -> list[Violation]:
     return out
 
 
+def validate_batch(specs, start_pos: np.ndarray, goal_pos: np.ndarray) -> list:
+    """``validate`` of B same-shape specs at once: the same violations, order and text per spec.
+
+    start_pos / goal_pos: (B, n, 3) positions (``engine.boundary_arrays``).  One vectorized
+    prefilter over every pair of every spec; only candidate pairs run the scalar expression.
+    """
+    B = len(specs)
+    out = [[] for _ in range(B)]
+    if B == 0:
+        return out
+    n = start_pos.shape[1]
+    geo = np.array([(s.geometry.l_xy, s.geometry.l_z) for s in specs], dtype=float)
+    scale = np.stack([1.0 / geo[:, 0], 1.0 / geo[:, 0], 1.0 / geo[:, 1]], axis=1)[:, None, :]
+    ii, jj = _pairs(n) if n > 1 else (np.zeros(0, int), np.zeros(0, int))
+    cand = {}
+    for label, P in (("start", start_pos), ("goal", goal_pos)):
+        if n > 1:
+            # |pi - pj|^2 = |pi|^2 + |pj|^2 - 2 pi.pj on the scaled positions (one batched matmul);
+            # a loose prefilter -- every candidate is re-checked with the exact scalar expression
+            Ps = np.ascontiguousarray(P) * scale
+            sq = np.einsum("bnk,bnk->bn", Ps, Ps)
+            d2 = sq[:, :, None] + sq[:, None, :] - 2.0 * np.matmul(Ps, Ps.transpose(0, 2, 1))
+            near = d2[:, ii, jj] < 1.0 + 1e-6 * (1.0 + sq[:, ii] + sq[:, jj])
+            for b, pk in zip(*np.nonzero(near)):
+                cand.setdefault(int(b), []).append((label, 0, int(ii[pk]), int(jj[pk])))
+    obs_any = any(s.obstacles for s in specs)
+    for b in range(B):
+        if b not in cand and not obs_any:
+            continue
+        spec = specs[b]
+        g = spec.geometry
+        entries = cand.get(b, [])
+        for label, P in (("start", start_pos), ("goal", goal_pos)):
+            for lab, _, i, j in entries:
+                if lab != label:
+                    continue
+                sep = _separation(P[b, i], P[b, j], g.l_xy, g.l_z)
+                if sep < 1.0:
+                    out[b].append(Violation(f"{label} pair ({i}, {j})", f"normalized separation {sep:.4f} < 1"))
+            for i in range(n):
+                for k, obs in enumerate(spec.obstacles):
+                    lxy, lz = obstacle_axes(spec, obs)
+                    sep = _separation(P[b, i], obs.center, lxy, lz)
+                    if sep < 1.0:
+                        out[b].append(Violation(f"{label} agent {i} vs obstacle {k}",
+                                                f"normalized separation {sep:.4f} < 1"))
+    return out
+
+
 # --- scenario JSON (reference problem.py:460-553) ---------------------------------------------
 
 
