@@ -578,6 +578,8 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   cfg.stream = s;
   cudaLaunchAttribute at[3];
   int na = 0;
+  cudaAccessPolicyWindow window = {};
+  bool has_window = false;
   at[na].id = cudaLaunchAttributeClusterDimension;
   at[na].val.clusterDim.x = L.C;
   at[na].val.clusterDim.y = 1;
@@ -618,12 +620,29 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       if (const char* hr = std::getenv("SWARM_L2_HIT")) at[na].val.accessPolicyWindow.hitRatio = (float)std::atof(hr);
       at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      ++na;
+      // As a stream attribute: measured on B200 the same window given as a launch attribute is
+      // not honoured (DRAM writes 86 GB vs 12 GB per 1024-scenario launch, profiles/l2_window_r2.txt).
+      // It is cleared again right after the launch, so the caller's stream keeps no window.
+      window = at[na].val.accessPolicyWindow;
+      has_window = true;
     }
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  ST_CUDA(cudaLaunchKernelEx(&cfg, L.fn, k));
+  if (has_window) {
+    cudaStreamAttrValue av = {};
+    av.accessPolicyWindow = window;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
+    cudaGetLastError();
+  }
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, L.fn, k);
+  if (has_window) {
+    cudaStreamAttrValue off = {};
+    off.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &off);
+    cudaGetLastError();
+  }
+  ST_CUDA(le);
   if (multi_ev) ST_CUDA(cudaEventRecord(multi_ev, s));
   // launches sharing this plan's workspaces (counter, slabs, exchange buffers) run in order,
   // whatever streams their callers use (advice r1: st_solve_device on several streams)
@@ -769,9 +788,11 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
   if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 8192 * sizeof(long long)));
   if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 8192 * sizeof(long long), s));
   k.tstamp = timers ? d_ts : nullptr;
-  // FP64: no persisting set-aside (the multipliers stream through L2 evict-first and the unit
-  // slots / positions need the whole cache); FP32: the multipliers fit and persist
-  if (!f32 || std::getenv("SWARM_NO_L2_PERSIST")) set_persisting_l2(pl->device, false);
+  // no persisting set-aside: FP64 multipliers stream through L2 evict-first and the unit slots /
+  // positions need the whole cache; FP32 multipliers (78 MB at n = 256) stay by their evict-last
+  // load policy alone (a persisting window measured 5.70 vs 5.61 ms on rand256_s0)
+  const bool persist = f32 && std::getenv("SWARM_L2_PERSIST_LARGE") != nullptr;
+  if (!persist) set_persisting_l2(pl->device, false);
   // grid-barrier kernels are serialized device-wide (see run())
   std::unique_lock<std::mutex> multi_lock(g_multi_mu);
   cudaEvent_t multi_ev = multi_event(pl->device);
@@ -784,7 +805,9 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   int na = 0;
-  if (f32 && !std::getenv("SWARM_NO_L2_PERSIST")) {
+  cudaAccessPolicyWindow window = {};
+  bool has_window = false;
+  if (persist) {
     // FP32 multipliers (n = 256: 78 MB) fit in L2: keep them there across iterations
     int max_persist = 0, max_window = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, pl->device);
@@ -799,12 +822,26 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
           (float)std::min(1.0, (double)max_persist / std::max<double>(1.0, at[na].val.accessPolicyWindow.num_bytes));
       at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      ++na;
+      window = at[na].val.accessPolicyWindow;  // as a stream attribute (see run())
+      has_window = true;
     }
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  ST_CUDA(cudaLaunchKernelEx(&cfg, le->fn, k));
+  if (has_window) {
+    cudaStreamAttrValue av = {};
+    av.accessPolicyWindow = window;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av);
+    cudaGetLastError();
+  }
+  const cudaError_t lerr = cudaLaunchKernelEx(&cfg, le->fn, k);
+  if (has_window) {
+    cudaStreamAttrValue off = {};
+    off.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &off);
+    cudaGetLastError();
+  }
+  ST_CUDA(lerr);
   ST_CUDA(cudaEventRecord(multi_ev, s));
   ST_CUDA(cudaEventRecord(pl->ev_done, s));
   if (timers) {
