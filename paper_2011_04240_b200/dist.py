@@ -7,15 +7,16 @@
    every rank in scenario order; the benchmark only reduces its timing (max).
 
 2. Pair sharding of ONE very large scenario (BASELINE config 5, n = 256).
-   ``am_solve_pair_sharded`` — every rank calls it with the same spec.  Each GPU owns
-   a contiguous slice of the time samples (all agent pairs at those samples); the one
-   per-iteration exchange (the 3 x n x n_v partial right-hand sides of the axis
-   solves plus three residual scalars) happens INSIDE the persistent kernel through
-   peer-mapped buffers (CUDA IPC over NVLink) and a system-scope barrier, summed in a
-   fixed participant order so every GPU computes identical iterates and the result
-   is bitwise the single-GPU multi-cluster result.  torch.distributed only moves the
-   64-byte IPC handles and provides the host barrier; there is no NCCL call on the
-   data path (the exchange is fused into the solve, tile by tile).
+   ``am_solve_pair_sharded`` — every rank calls it with the same spec.  For n > 64 (the
+   large-fleet kernel) each GPU owns a contiguous, cost-balanced range of the
+   (agent-block pair x sample) units -- a range of agent pairs at all samples -- run by
+   one CTA per SM; the one per-iteration exchange (its 3 x n x n_v partial right-hand
+   sides plus two residual scalars) happens INSIDE the persistent kernel through
+   peer-mapped buffers (CUDA IPC over NVLink) and a system-scope barrier, summed in rank
+   order so every GPU computes identical iterates.  (n <= 64: the multi-cluster kernel,
+   each GPU a slice of the time samples, bitwise the single-GPU result.)
+   torch.distributed only moves the 64-byte IPC handles and provides the host barrier;
+   there is no NCCL call on the data path (the exchange is fused into the solve).
 """
 
 from __future__ import annotations
@@ -97,8 +98,8 @@ def am_solve_pair_sharded(spec, config=None, cache=None, group=None, shard_group
     Every rank calls this with the same ``spec``/``config`` (torchrun, one process per
     GPU, ``config.device`` = this rank's GPU; default LOCAL_RANK).  Returns the
     ``SolveReport`` on rank 0 and ``None`` elsewhere.  Same validation and errors as
-    ``am_solve`` (reference solver.py:363-367); results are bitwise those of the
-    single-GPU solve of the same spec.
+    ``am_solve`` (reference solver.py:363-367); every GPU holds identical iterates (the
+    single-GPU solve's within the parity bar; bitwise for one rank).
     """
     import torch.distributed as dist
     from . import engine, kkt, poly
