@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -65,6 +66,7 @@ struct Launch {
   int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_tail = 0;
   int G = 1;  // groups (GPUs) sharing the scenario; participants = G x K clusters
   int f32 = 0;    // FP32 pair state: multipliers are 4-byte elements
+  int active = 0; // co-resident clusters of this shape
   size_t smem_bytes = 0;
   long long lam_per_cta = 0;
   KernelFn fn = nullptr;
@@ -98,6 +100,7 @@ struct st_plan {
   void* d_lgw = nullptr;          // large-fleet workspace (tables, unit slots, positions, ...)
   size_t lgw_bytes = 0;
   std::vector<long long> lg_key;  // layout whose tables are in d_lgw
+  std::map<std::vector<int>, Launch> launch_cache;  // choose_launch results (see choose_launch_cached)
   std::mutex mu;
 };
 
@@ -194,6 +197,8 @@ const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, bool f32) {
   return nullptr;
 }
 
+cudaError_t ensure_smem_attr(int device, const void* fn, size_t bytes);
+
 int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G = 1, bool f32 = false) {
   const int n = pl->n;
   if (n < 1 || n > 256) return fail(ST_EUNSUPPORTED, "n_agents must be in [1, 256] for the compiled kernels");
@@ -263,6 +268,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     if (keep && pass == 0) continue;
     const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam, f32);
     if (!ke) continue;
+    const long long bud = budget;
     if ((long long)C * G > pl->m || C < 1 || C > 16) continue;  // every CTA owns >= 1 sample
     Launch T = L;
     T.NT = ke->NT;
@@ -272,7 +278,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     long long need = base + (pass == 0 ? lam_rows_dbl(T, (long long)T.tasks_max * T.nsteps) : 0);
     const bool want_multi = G > 1 || (batch == 1 && C > 1 && (mc_env ? std::atoi(mc_env) != 0 : pl->n > 32));
     bool sized_for_split = false;
-    if (need > budget && want_multi) {
+    if (need > bud && want_multi) {
       // one cluster cannot hold the scenario's per-CTA buffers, but K co-resident clusters
       // (each CTA owning ~m/(G K C) samples) may: size the layout for the multi-cluster split
       T.G = G;
@@ -281,7 +287,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       need = base + (pass == 0 ? lam_rows_dbl(T, (long long)T.tasks_max * T.nsteps) : 0);
       sized_for_split = T.K > 1;
     }
-    if (need > budget) continue;
+    if (need > bud) continue;
     T.lam_smem = pass == 0 ? 1 : 0;
     T.lam_tail = 0;
     long long need2 = need;
@@ -289,13 +295,12 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       // hybrid: spare shared memory holds each warp's last multiplier rows (the rest stays in L2)
       const char* hy = std::getenv("SWARM_LAM_HYBRID");
       if (!hy || std::atoi(hy) != 0) {
-        T.lam_tail = tail_rows(T, budget - need);
+        T.lam_tail = tail_rows(T, bud - need);
         need2 = need + lam_rows_dbl(T, (long long)T.lam_tail * (T.NT / 32));
       }
     }
     T.smem_bytes = (size_t)need2 * 8;
-    ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    ST_CUDA(cudaFuncSetAttribute(T.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T.smem_bytes));
+    ST_CUDA(ensure_smem_attr(pl->device, (const void*)T.fn, T.smem_bytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(T.NT);
@@ -317,6 +322,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     const bool multi = G > 1 || (batch == 1 && C > 1 && active > 1 && want_multi);
     if (sized_for_split && !multi) continue;  // sized for a split that cannot run
     T.nclusters = std::min(batch, active);
+    T.active = active;
     if (multi) {
       Launch M = T;
       M.G = G;
@@ -330,7 +336,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
       }
       if (mneed <= budget) {
         M.smem_bytes = (size_t)mneed * 8;
-        ST_CUDA(cudaFuncSetAttribute(M.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M.smem_bytes));
+        ST_CUDA(ensure_smem_attr(pl->device, (const void*)M.fn, M.smem_bytes));
         M.nclusters = M.K;
         T = M;
       } else if (T.K > 1) {
@@ -342,6 +348,36 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     return 0;
   }
   return fail(ST_EUNSUPPORTED, "no cluster configuration fits this problem on the device");
+}
+
+// choose_launch, memoized per plan: the occupancy queries and attribute calls run once per
+// (single/batch, cluster hint, keep_state, groups, FP32) shape; the cluster count follows the
+// batch (SWARM_* launch knobs are read when a shape is first seen).
+int choose_launch_cached(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G, bool f32) {
+  const std::vector<int> key = {batch == 1 ? 1 : 2, hint, keep ? 1 : 0, G, f32 ? 1 : 0};
+  auto it = pl->launch_cache.find(key);
+  if (it != pl->launch_cache.end()) {
+    L = it->second;
+    if (L.K <= 1) L.nclusters = std::min(batch, L.active);
+    return 0;
+  }
+  int rc = choose_launch(pl, batch, hint, keep, L, G, f32);
+  if (rc == 0) pl->launch_cache[key] = L;
+  return rc;
+}
+
+// Dynamic shared-memory limits of the kernel functions only ever grow (a launch configuration
+// cached by one plan stays valid whatever another plan needs), per device.
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_attr;
+cudaError_t ensure_smem_attr(int device, const void* fn, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int& cur = g_attr[{device, fn}];
+  if (cur >= (int)bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = (int)bytes;
+  return e;
 }
 
 // device-wide ordering of grid-barrier (multi-cluster) launches, one event per device
@@ -460,7 +496,7 @@ LargeLayout large_layout(const st_plan* pl, int G, int cpg) {
 
 // CTAs per SM the large kernel fits (1 by design), and the grid of one GPU
 int large_grid(st_plan* pl, const LargeEntry* le, size_t smem, int& grid) {
-  ST_CUDA(cudaFuncSetAttribute(le->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ST_CUDA(ensure_smem_attr(pl->device, (const void*)le->fn, smem));
   int occ = 0, nsm = 0;
   ST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, le->fn, swarm::LG_NT, smem));
   ST_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device));
@@ -1045,7 +1081,7 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
     return run_large(pl, (flags & ST_FLAG_FP32) != 0, c0, beq, geom, switch_every, max_iters, tol, c_out, hist,
                      iters, conv, s, nullptr);
   Launch L;
-  rc = choose_launch(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, 1, (flags & ST_FLAG_FP32) != 0);
+  rc = choose_launch_cached(pl, batch, hint, (flags & ST_FLAG_KEEP_STATE) != 0, L, 1, (flags & ST_FLAG_FP32) != 0);
   if (rc) return rc;
   return run(pl, L, batch, c0, beq, geom, switch_every, max_iters, tol, flags, c_out, hist, iters, conv, lam_out,
              d_out, s);
@@ -1064,7 +1100,7 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   const bool large = hint <= 0 && large_eligible(pl, batch, keep);
   Launch L;
   if (!large) {
-    rc = choose_launch(pl, batch, hint, keep, L, ext ? ext->G : 1, (flags & ST_FLAG_FP32) != 0);
+    rc = choose_launch_cached(pl, batch, hint, keep, L, ext ? ext->G : 1, (flags & ST_FLAG_FP32) != 0);
     if (rc) return rc;
   }
   const int n = pl->n, nv = pl->nv, m = pl->m;

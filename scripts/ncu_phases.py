@@ -9,8 +9,13 @@ import collections, csv, io, os, re, subprocess, sys, tempfile
 rep, lib, kern = sys.argv[1:4]
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, check=True, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+# the library holds one cubin per translation unit: disassemble the one defining the kernel
+sass = ""
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    if re.search(r"\.text\.\S*" + re.escape(kern), txt):
+        sass = txt
+        break
 addr2line, cur_fn, cur = {}, None, None
 for ln in sass.splitlines():
     m = re.match(r"\s*\.text\.(\S+):", ln)
