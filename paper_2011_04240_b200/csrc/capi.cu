@@ -63,7 +63,7 @@ const KernelEntry kKernels[] = {
 struct Launch {
   int NVMAX = 0;
   int NB = 0, NT = 0, W = 0, C = 0, nsteps = 0, tmax = 0, tasks_max = 0, own_max = 0;
-  int lam_smem = 0, nclusters = 0, qslots = 0, wpg = 0, c_global = 0, K = 1, lam_tail = 0;
+  int lam_smem = 0, nclusters = 0, c_global = 0, K = 1, lam_tail = 0;
   int G = 1;  // groups (GPUs) sharing the scenario; participants = G x K clusters
   int f32 = 0;    // FP32 pair state: multipliers are 4-byte elements
   int active = 0; // co-resident clusters of this shape
@@ -131,49 +131,63 @@ long long layout(st_plan* pl, Launch& L, int C) {
   const int KC = L.G * L.K * C;  // CTAs sharing one scenario
   L.tmax = ceil_div(pl->m, KC);
   L.tasks_max = ceil_div(L.tmax, TPW);  // time groups of the largest CTA
-  // A CTA owns floor(m/C) or ceil(m/C) samples; its warps split groups x steps evenly
-  // (work_split), so bound the slot counts over both cases.
-  L.qslots = 1;
-  L.wpg = 1;
-  for (int tc : {pl->m / KC, L.tmax}) {
-    if (tc < 1) continue;
-    const int spw = ceil_div(ceil_div(tc, TPW) * L.nsteps, NW);
-    L.qslots = std::max(L.qslots, ceil_div(spw, L.nsteps) + 1);         // groups a warp can touch
-    L.wpg = std::max(L.wpg, std::min(NW, ceil_div(L.nsteps, spw) + 1));  // warps sharing one group
-  }
-  L.own_max = ceil_div(n, C);
+  // redundant solve (every CTA solves all agents, one cluster barrier per iteration) for small
+  // single-cluster launches; wide clusters and multi-cluster launches use owners + all-gather
+  const char* re = std::getenv("SWARM_RED");
+  k.red = (L.G * L.K == 1 && !L.c_global && C <= 4 && (!re || std::atoi(re) != 0)) ? 1 : 0;
+  L.own_max = k.red ? n : ceil_div(n, C);
+  const int NV = L.NVMAX;
+  const bool obst = pl->nobs > 0;
+  // partial S'b rows j*3 + ax (+ 3 agent-sum rows); row stride == 4 (mod 8) doubles keeps the
+  // DMMA operand loads of project_phase bank-conflict free
+  int nrp = 3 * n + (obst ? 3 : 0);
+  nrp += nrp & 1;
+  while (nrp % 8 != 4) nrp += 2;
+  k.nrow_p = nrp;
+  k.xs = 3 * NP + 8;  // X group stride == 8 (mod 16): conflict-free 16-byte stores of DMMA tiles
   long long o = 0;
   auto take = [&](int& off, long long cnt) {
     off = (int)o;
     o += (cnt + 1) & ~1LL;  // keep 16-byte alignment
   };
-  const int NV = L.NVMAX;
   take(k.o_c, L.c_global ? 0 : 3LL * n * NV);
-  // Regions never live at the same time share storage:
-  //   qp (pairwise -> combine) and Rp (projection -> owners' pull, before the next pairwise)
-  //   X (positions -> pairwise) and qc (combine -> projection)
-  const long long qp_sz = (long long)NW * L.qslots * 3 * NP, rp_sz = 3LL * n * NV;
-  take(k.o_qp, std::max(qp_sz, rp_sz));
-  k.o_Rp = k.o_qp;
-  take(k.o_qsp, (long long)NW * L.qslots * 3 * TPW);
-  const long long x_sz = (long long)L.tasks_max * 3 * NP, qc_sz = (long long)L.tmax * ((3LL * n + 1) & ~1LL) + 3LL * L.tmax;
-  take(k.o_X, std::max(x_sz, qc_sz));
-  k.o_qc = k.o_X;
-  take(k.o_tab, ((long long)L.tmax * (2 + 2 * L.wpg) + 1) / 2);
-  take(k.o_P, (long long)L.tmax * NV);
-  take(k.o_xch, 3LL * NV + 4);  // agent sums | sum r^2, max |r| | boundary max x 2 parities
+  // the DMMA tiles read whole 4-row (qv) and 8-row (P) blocks: rows past the CTA's samples are zero
+  k.qrow = (L.tmax + 3) / 4 * 4;
+  k.prow = (L.tasks_max * TPW + 7) / 8 * 8 + 8;
+  take(k.o_qv, (long long)k.qrow * nrp);  // first warp of each group: rows per time
+  // exchange region Rp [3n][NV] | xch [agent sums 3 NV | sum r^2, max |r| | 2 spare].
+  // Owner mode: it aliases the qx slots (dead after project_phase's fix-up; the owners pull it
+  // between the two cluster barriers).  red: two parity copies of its own (one barrier).
+  const long long rx = (3LL * n * NV + 3LL * NV + 4 + 1) & ~1LL, qx_sz = (long long)NW * TPW * nrp;
+  if (k.red) {
+    take(k.o_qx, qx_sz);  // warps starting inside a group: their first group's rows
+    take(k.o_Rp, 2 * rx);
+  } else {
+    take(k.o_qx, std::max(qx_sz, rx));
+    k.o_Rp = k.o_qx;
+  }
+  k.o_xch = k.o_Rp + 3 * n * NV;
   k.xch_norm = 3 * NV;
-  take(k.o_cown, (long long)L.own_max * 3 * NV);
+  k.rx = k.red ? (int)rx : 0;
+  take(k.o_X, (long long)L.tasks_max * k.xs);
+  take(k.o_tab, (L.tmax + 1) / 2);
+  take(k.o_P, (long long)k.prow * NV);
+  take(k.o_cown, k.red ? 0 : (long long)L.own_max * 3 * NV);
   take(k.o_nrm, 3LL * C);
   take(k.o_otab, (n + 1) / 2);
-  take(k.o_R, (long long)L.own_max * 3 * NV);
+  take(k.o_R, !k.red ? (long long)L.own_max * 3 * NV
+               : 3LL * n * (NV == 12 ? swarm::SolveOp<12>::kas(obst) : swarm::SolveOp<16>::kas(obst)));
   take(k.o_Rb, 3LL * NV);
   take(k.o_mat, NV == 12 ? swarm::StageMats<12>::SIZE : swarm::StageMats<16>::SIZE);
+  take(k.o_sa, !k.red ? 0
+               : NV == 12 ? swarm::SolveOp<12>::MA * swarm::SolveOp<12>::kas(obst)
+                          : swarm::SolveOp<16>::MA * swarm::SolveOp<16>::kas(obst));
   take(k.o_geo, 8 + 8LL * pl->nobs);
   take(k.o_beq, 18LL * L.own_max);
   take(k.o_bb, 18);
   take(k.o_wp, 2LL * NW);
   take(k.o_misc, 2);
+  take(k.o_bnd, 2);
   k.o_lam = (int)o;
   L.lam_per_cta = (long long)L.tasks_max * L.nsteps * 96;
   return o;
@@ -528,7 +542,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   k.P = pl->P; k.G = pl->G; k.Gm = pl->Gm; k.F = pl->F; k.Fm = pl->Fm; k.E = pl->E; k.rho = pl->rho;
   k.mats = pl->mats; k.inv_rho = pl->inv_rho;
   k.C = L.C; k.W = L.W; k.nsteps = L.nsteps; k.tmax = L.tmax; k.tasks_max = L.tasks_max;
-  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta; k.qslots = L.qslots; k.wpg = L.wpg;
+  k.own_max = L.own_max; k.lam_in_smem = L.lam_smem; k.lam_per_cta = L.lam_per_cta;
   k.lam_tail = L.lam_tail;
   k.B = batch; k.gstride = 2 + 5 * pl->nobs;
   k.c0 = c0; k.beq = beq; k.geom = geom; k.c_out = c_out; k.hist = hist; k.iters = iters; k.conv = conv;
