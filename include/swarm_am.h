@@ -83,6 +83,30 @@ int st_solve(st_plan* plan, int batch, const double* c0, const double* b_eq, con
              double* c_out, double* hist, int* iters, int* converged, double* lam_out,
              double* d_out, float* timings_ms);
 
+/* st_solve plus the report's post-loop work in the same call, on the device (replaces
+ * SolveReport.trajectories = c_axis @ P.T, solver.py:133-136, and _final_metrics,
+ * solver.py:497-509 -> validation.py:39-132): keep_state is not available here.
+ *   traj     batch x n x m x 3   sampled positions (report layout)
+ *   arc      batch x n           arc length per agent (validation.py:96-108)
+ *   smooth   batch x n           smoothness per agent (validation.py:111-121)
+ *   min_dist batch               minimum normalized distance (+inf without rows)
+ *   n_viol   batch               number of violations (< 1) of the collision check
+ *   col_geom batch x 2 (l_xy, l_z) and col_obs batch x n_obs x 5 as for
+ *            st_check_collisions_batch (needed for min_dist / n_viol).
+ * Any of the five outputs may be NULL.  The verdict is computed on the device
+ * trajectories; positions and sums use a fixed FMA/summation order (agreement with
+ * the host formulas to rounding). */
+int st_solve_report(st_plan* plan, int batch, const double* c0, const double* b_eq, const double* geom,
+                    int switch_every, int max_iters, double tol, int flags, int cluster_hint, double* c_out,
+                    double* hist, int* iters, int* converged, float* timings_ms, const double* col_geom,
+                    const double* col_obs, double* traj, double* arc, double* smooth, double* min_dist,
+                    long long* n_viol);
+
+/* Page-locked host memory for output arrays (device-to-host copies at full link speed;
+ * the Python binding pools these buffers for the report trajectories). */
+int st_host_alloc(long long bytes, void** out);
+int st_host_free(void* ptr);
+
 /* Same contract, every array a device pointer, enqueued on `stream`
  * (a cudaStream_t, NULL = the plan's stream); no host synchronization. */
 int st_solve_device(st_plan* plan, int batch, const double* c0, const double* b_eq,

@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "_swarm_am.so")
 # so the (independent, slow) device compilations run in parallel
 SOURCES = [os.path.join(CSRC, f) for f in ("capi.cu", "inst_nb1_12.cu", "inst_nb1_16.cu", "inst_nb2.cu",
                                            "inst_nb48.cu", "inst_f32_nb1.cu", "inst_f32_nb248.cu",
-                                           "inst_large.cu", "collisions.cu")]
+                                           "inst_large.cu", "collisions.cu", "report.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "am_kernel.cuh"), os.path.join(CSRC, "am_large.cuh"),
                   os.path.join(ROOT, "include", "swarm_am.h")]
 

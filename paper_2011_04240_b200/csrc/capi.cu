@@ -77,6 +77,24 @@ struct Launch {
 
 // shared with collisions.cu
 int swarm_fail(int code, const std::string& msg) { return fail(code, msg); }
+// report.cu / collisions.cu: the device-side report pass of st_solve_report
+size_t swarm_report_smem(int m);
+cudaError_t swarm_report_launch(int B, int n, int m, int nv, int nvp, const double* c, const double* P, double* traj,
+                                double* arc, double* smooth, cudaStream_t s);
+cudaError_t swarm_collision_summary_launch(int B, int n, int m, const double* d_traj, const double* d_geom, int n_obs,
+                                           const double* d_obs, int* row_cnt, unsigned long long* min_total,
+                                           cudaStream_t s);
+
+// outputs of the report pass (st_solve_report); any output may be NULL
+struct ReportReq {
+  const double* geom2;  // batch x 2: l_xy, l_z of the collision check
+  const double* obs;    // batch x n_obs x 5: cx, cy, cz, l_xy/2 + r, l_z/2 + r
+  double* traj;         // batch x n x m x 3
+  double* arc;          // batch x n
+  double* smooth;       // batch x n
+  double* min_dist;     // batch
+  long long* n_viol;    // batch
+};
 
 struct st_plan {
   int n, nobs, m, nv, S, device, nvmax;
@@ -97,6 +115,8 @@ struct st_plan {
   int smem_sm = 0;  // shared memory per SM
   int persist_set = 0;
   cudaEvent_t ev_done = nullptr;  // last launch that used this plan's workspaces
+  void* d_rep = nullptr;          // st_solve_report workspace (trajectories, metrics, verdict rows)
+  size_t rep_bytes = 0;
   void* d_lgw = nullptr;          // large-fleet workspace (tables, unit slots, positions, ...)
   size_t lgw_bytes = 0;
   std::vector<long long> lg_key;  // layout whose tables are in d_lgw
@@ -1064,6 +1084,7 @@ int st_plan_destroy(st_plan* pl) {
   if (pl->d_rg) cudaFree(pl->d_rg);
   if (pl->d_io) cudaFree(pl->d_io);
   if (pl->d_lgw) cudaFree(pl->d_lgw);
+  if (pl->d_rep) cudaFree(pl->d_rep);
   if (pl->stream) cudaStreamDestroy(pl->stream);
   delete pl;
   return ST_OK;
@@ -1103,7 +1124,7 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
 
 static int solve_host(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom, int switch_every,
              int max_iters, double tol, int flags, int hint, double* c_out, double* hist, int* iters, int* conv,
-             double* lam_out, double* d_out, float* timings, const ShardExt* ext) {
+             double* lam_out, double* d_out, float* timings, const ShardExt* ext, const ReportReq* rep = nullptr) {
   int rc = check_common(pl, batch, switch_every, max_iters, tol, flags);
   if (rc) return rc;
   if (!c0 || !beq || !geom || !c_out || !hist || !iters || !conv) return fail(ST_EINVAL, "NULL buffer");
@@ -1149,6 +1170,46 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
                    keep ? d_lam : nullptr, keep ? d_dd : nullptr, s, ext);
   if (rc) return rc;
   ST_CUDA(cudaEventRecord(pl->ev[2], s));
+  std::vector<unsigned long long> mt;
+  if (rep) {
+    // report pass on the device: trajectories, arc length / smoothness, collision summary
+    const int n_obs = pl->nobs;
+    const long long n_rows = (long long)n * (n - 1) / 2 + (long long)n * n_obs;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t b_traj = al((size_t)batch * n * m * 24), b_met = al((size_t)batch * n * 16),
+                 b_geom = al((size_t)batch * 16), b_obs = al((size_t)batch * n_obs * 40 + 8),
+                 b_cnt = al((size_t)batch * n_rows * 4 + 4), b_mt = al((size_t)batch * 16);
+    const size_t rneed = b_traj + b_met + b_geom + b_obs + b_cnt + b_mt;
+    if (rneed > pl->rep_bytes) {
+      if (pl->d_rep) cudaFree(pl->d_rep);
+      pl->d_rep = nullptr;
+      pl->rep_bytes = 0;
+      ST_CUDA(cudaMalloc(&pl->d_rep, rneed));
+      pl->rep_bytes = rneed;
+    }
+    char* q = (char*)pl->d_rep;
+    double* r_traj = (double*)q;
+    double* r_arc = (double*)(q += b_traj);
+    double* r_smooth = r_arc + (size_t)batch * n;
+    double* r_geom = (double*)(q += b_met);
+    double* r_obs = (double*)(q += b_geom);
+    int* r_cnt = (int*)(q += b_obs);
+    unsigned long long* r_mt = (unsigned long long*)(q += b_cnt);
+    const bool verdict = rep->min_dist || rep->n_viol;
+    if (verdict) {
+      ST_CUDA(cudaMemcpyAsync(r_geom, rep->geom2, (size_t)batch * 16, cudaMemcpyHostToDevice, s));
+      if (n_obs) ST_CUDA(cudaMemcpyAsync(r_obs, rep->obs, (size_t)batch * n_obs * 40, cudaMemcpyHostToDevice, s));
+    }
+    ST_CUDA(swarm_report_launch(batch, n, m, nv, pl->nvmax, d_cout, pl->P, r_traj, r_arc, r_smooth, s));
+    if (verdict) {
+      ST_CUDA(swarm_collision_summary_launch(batch, n, m, r_traj, r_geom, n_obs, r_obs, r_cnt, r_mt, s));
+      mt.resize(2 * (size_t)batch);
+      ST_CUDA(cudaMemcpyAsync(mt.data(), r_mt, (size_t)batch * 16, cudaMemcpyDeviceToHost, s));
+    }
+    if (rep->traj) ST_CUDA(cudaMemcpyAsync(rep->traj, r_traj, (size_t)batch * n * m * 24, cudaMemcpyDeviceToHost, s));
+    if (rep->arc) ST_CUDA(cudaMemcpyAsync(rep->arc, r_arc, (size_t)batch * n * 8, cudaMemcpyDeviceToHost, s));
+    if (rep->smooth) ST_CUDA(cudaMemcpyAsync(rep->smooth, r_smooth, (size_t)batch * n * 8, cudaMemcpyDeviceToHost, s));
+  }
   ST_CUDA(cudaMemcpyAsync(c_out, d_cout, n_c * 8, cudaMemcpyDeviceToHost, s));
   ST_CUDA(cudaMemcpyAsync(hist, d_hist, n_h * 8, cudaMemcpyDeviceToHost, s));
   ST_CUDA(cudaMemcpyAsync(iters, d_it, batch * 4, cudaMemcpyDeviceToHost, s));
@@ -1165,6 +1226,14 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     ST_CUDA(cudaEventElapsedTime(&timings[1], pl->ev[1], pl->ev[2]));
     ST_CUDA(cudaEventElapsedTime(&timings[2], pl->ev[2], pl->ev[3]));
   }
+  if (rep && !mt.empty()) {
+    for (int b = 0; b < batch; ++b) {
+      double mn;
+      memcpy(&mn, &mt[b], 8);
+      if (rep->min_dist) rep->min_dist[b] = mn;
+      if (rep->n_viol) rep->n_viol[b] = (long long)mt[batch + b];
+    }
+  }
   return ST_OK;
 }
 
@@ -1173,6 +1242,36 @@ int st_solve(st_plan* pl, int batch, const double* c0, const double* beq, const 
              double* lam_out, double* d_out, float* timings) {
   return solve_host(pl, batch, c0, beq, geom, switch_every, max_iters, tol, flags, hint, c_out, hist, iters, conv,
                     lam_out, d_out, timings, nullptr);
+}
+
+int st_solve_report(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom,
+                    int switch_every, int max_iters, double tol, int flags, int hint, double* c_out, double* hist,
+                    int* iters, int* conv, float* timings, const double* col_geom, const double* col_obs,
+                    double* traj, double* arc, double* smooth, double* min_dist, long long* n_viol) {
+  if (!pl) return fail(ST_EINVAL, "NULL plan");
+  if ((min_dist || n_viol) && (!col_geom || (pl->nobs > 0 && !col_obs)))
+    return fail(ST_EINVAL, "collision geometry missing");
+  if (batch > 65535) return fail(ST_EINVAL, "report pass: batch larger than 65535 scenarios");
+  if (pl->m < 1 || swarm_report_smem(pl->m) > (size_t)pl->smem_optin)
+    return fail(ST_EUNSUPPORTED, "report pass: too many samples per trajectory for one warp's shared memory");
+  if (flags & ST_FLAG_KEEP_STATE) return fail(ST_EINVAL, "report pass: keep_state solves use st_solve");
+  const ReportReq rep{col_geom, col_obs, traj, arc, smooth, min_dist, n_viol};
+  return solve_host(pl, batch, c0, beq, geom, switch_every, max_iters, tol, flags, hint, c_out, hist, iters, conv,
+                    nullptr, nullptr, timings, nullptr, &rep);
+}
+
+// Page-locked host buffers (report outputs): device-to-host copies at full PCIe/C2C speed.
+int st_host_alloc(long long bytes, void** out) {
+  if (!out || bytes < 0) return fail(ST_EINVAL, "bad arguments");
+  *out = nullptr;
+  if (bytes == 0) return ST_OK;
+  ST_CUDA(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+  return ST_OK;
+}
+
+int st_host_free(void* ptr) {
+  if (ptr) ST_CUDA(cudaFreeHost(ptr));
+  return ST_OK;
 }
 
 // ---- pair-sharded solves over G GPUs (one process per GPU, peer-mapped group buffers)

@@ -229,6 +229,29 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
+__global__ void init_summary_kernel(unsigned long long* min_total, int B) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    min_total[b] = 0x7ff0000000000000ULL;  // +inf
+    min_total[B + b] = 0;
+  }
+}
+
+// Device-resident verdict summary for st_solve_report (capi.cu): per scenario the minimum
+// normalized distance (bits, min_total[b]) and the violation count (min_total[B + b]) of the
+// B x n x m x 3 trajectories already on the device; row_cnt: B x n_rows scratch.
+cudaError_t swarm_collision_summary_launch(int B, int n, int m, const double* d_traj, const double* d_geom, int n_obs,
+                                           const double* d_obs, int* row_cnt, unsigned long long* min_total,
+                                           cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  init_summary_kernel<<<(B + 255) / 256, 256, 0, s>>>(min_total, B);
+  const long long n_pairs = (long long)n * (n - 1) / 2, n_rows = n_pairs + (long long)n * n_obs;
+  if (n_rows == 0 || m == 0) return cudaGetLastError();
+  Rows R{d_traj, d_obs, d_geom, n, m, n_obs, n_pairs, n_rows};
+  const dim3 grid((unsigned)((n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock), (unsigned)B);
+  rows_kernel<<<grid, kWarpsPerBlock * 32, 0, s>>>(R, row_cnt, min_total, min_total + B);
+  return cudaGetLastError();
+}
+
 extern "C" int st_check_collisions_batch(int B, int n, int m, const double* traj, const double* geom, int n_obs,
                                          const double* obs, int device, long long cap, int* ids, double* vals,
                                          double* min_out, long long* total_out) {

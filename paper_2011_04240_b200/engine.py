@@ -18,6 +18,7 @@ launch (the reference runs those through a thread pool, bench.py:120-158).
 
 from __future__ import annotations
 
+import gc
 import itertools
 import logging
 import math
@@ -423,53 +424,68 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
                   foreign=None) -> list:
     """Device outputs of one launch -> one SolveReport per scenario (reference field layout).
 
-    Whole-batch array work (trajectories, collision verdicts, arc length / smoothness) is done
-    once for all scenarios; single solves take the same path with B = 1, so batch and single
-    solves report identical trajectories and metrics."""
+    Whole-batch array work is done once for all scenarios: with the device report pass
+    (``st_solve_report``, ``out["traj"]``) the trajectories, arc length / smoothness and the
+    collision summary come from the device; otherwise (keep_state, m < 3) the trajectories
+    are formed on the host as the reference does (c_axis @ P.T) and the metrics from the
+    coefficients.  Single solves take the same path with B = 1, so batch and single solves
+    report identical trajectories and metrics."""
     t0, t1, t2, t3 = stamps
     h2d_ms, loop_ms, d2h_ms = out["timings_ms"]
     B = len(specs)
     n = len(specs[0].start)
     nv, m = basis.num_coeffs, basis.num_samples
-    # trajectories = c_axis @ P.T per axis (solver.py:133-136), all scenarios and axes in one product
     c = out["c"]
-    trajs = np.ascontiguousarray((c.reshape(-1, nv) @ basis.P.T).reshape(B, 3, n, m).transpose(0, 2, 3, 1))
     tc0 = time.perf_counter()
+    if "traj" in out:
+        trajs = out["traj"]
+    else:
+        # trajectories = c_axis @ P.T per axis (solver.py:133-136), all scenarios and axes in one product
+        trajs = np.ascontiguousarray((c.reshape(-1, nv) @ basis.P.T).reshape(B, 3, n, m).transpose(0, 2, 3, 1))
     if with_metrics:
-        cols = metrics.collision_summary_device_batch(trajs, specs, _opt(config, "device", 0))
-        arc, smooth = metrics.trajectory_metrics_batch_coeffs(c, basis.P)
+        if "min_dist" in out:
+            mins, counts = out["min_dist"].tolist(), out["n_viol"].tolist()
+            arc, smooth = out["arc"], out["smooth"]
+        else:
+            cols = metrics.collision_summary_device_batch(trajs, specs, _opt(config, "device", 0))
+            mins, counts = [x[0] for x in cols], [x[1] for x in cols]
+            arc, smooth = metrics.trajectory_metrics_batch_coeffs(c, basis.P)
         arc_l, smooth_l = arc.tolist(), smooth.tolist()
         arc_mean, smooth_mean = arc.mean(axis=1).tolist(), smooth.mean(axis=1).tolist()
     metrics_s = (time.perf_counter() - tc0) / B
     iters = out["iters"].tolist()
     conv = out["converged"].tolist()
-    hist = out["hist"]
+    hist = out["hist"].tolist()  # one conversion for the whole batch; histories are list slices
     common = {"assembly_s": t1 - t0, "factorization_s": t2 - t1, "loop_s": loop_ms / 1e3, "h2d_s": h2d_ms / 1e3,
               "d2h_s": d2h_ms / 1e3, "solve_call_s": t3 - t2, "metrics_s": metrics_s, "batch": B}
+    loop_s = loop_ms / 1e3
+    stats_obj = foreign if foreign is not None else cache
     reports = []
-    for b, spec in enumerate(specs):
-        it = int(iters[b])
-        before = cache.stats()
+    for b in range(B):
+        it = iters[b]
+        before = cache.stats() if foreign is not None else None
         cache.count_solve(3 * it)
         _sync_foreign(cache, foreign, before)
         coeffs = c[b]
         rep_metrics = {}
         if with_metrics:
-            md, count = cols[b]
+            md = mins[b]
             rep_metrics = {
                 "min_normalized_distance": None if math.isinf(md) else md,
-                "num_collision_violations": count,
+                "num_collision_violations": counts[b],
                 "arc_length": arc_l[b],
                 "smoothness": smooth_l[b],
                 "mean_arc_length": arc_mean[b],
                 "mean_smoothness": smooth_mean[b],
             }
-        h = hist[b, :, :it]
+        h0, h1, h2 = hist[b]
+        h0, h1, h2 = h0[:it], h1[:it], h2[:it]
         timings = dict(common)
-        timings["per_iteration_s"] = loop_ms / 1e3 / max(1, it)
+        timings["per_iteration_s"] = loop_s / max(1, it)
         timings["total_s"] = time.perf_counter() - t0
         diagnostics = {}
         if config.keep_state:
+            spec = specs[b]
             _, lxy, lz, alpha, beta = _pair_state(spec, coeffs, basis)
             lam = out["lam"]
             stage = schedule.stage_for(it - 1)
@@ -478,21 +494,21 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
                 pair_vars=PairVariables(alpha=alpha, beta=beta, d=out["d"]),
                 multipliers=Multipliers(lambda_x=lam[0], lambda_y=lam[1], lambda_z=lam[2]),
                 rho=schedule.values[stage], stage=stage, iteration=it,
-                residual_norms=h[0].tolist(), residual_max=h[1].tolist(),
+                residual_norms=list(h0), residual_max=list(h1),
                 system=SystemView(spec, basis))
         reports.append(SolveReport(
             trajectories=trajs[b],
             coefficients=coeffs,
             converged=bool(conv[b]),
             iterations=it,
-            residual_norm=float(h[0, -1]) if it else 0.0,
-            residual_max_abs=float(h[1, -1]) if it else 0.0,
-            residual_norm_history=h[0].tolist(),
-            residual_max_history=h[1].tolist(),
-            boundary_max_history=h[2].tolist(),
+            residual_norm=h0[-1] if it else 0.0,
+            residual_max_abs=h1[-1] if it else 0.0,
+            residual_norm_history=h0,
+            residual_max_history=h1,
+            boundary_max_history=h2,
             timings=timings,
             metrics=rep_metrics,
-            cache_stats=(foreign if foreign is not None else cache).stats(),
+            cache_stats=stats_obj.stats(),
             diagnostics=diagnostics,
         ))
     return reports
@@ -500,7 +516,68 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
 
 def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorCache | None = None,
                    with_metrics: bool = True) -> list:
-    """Solve scenarios sharing one fingerprint in one device launch; one report each."""
+    """Solve scenarios sharing one fingerprint in one device launch; one report each.
+
+    The host work builds O(B) small containers (state tuples, history lists, reports) that
+    the cyclic garbage collector would otherwise re-traverse many times over; none of them
+    forms cycles, so collection is paused for the call (restored on exit)."""
+    was_enabled = gc.isenabled()
+    gc.disable()
+    try:
+        return _am_solve_batch(specs, config, cache, with_metrics)
+    finally:
+        if was_enabled:
+            gc.enable()
+
+
+# Large batches on the device report path run as a pipeline of contiguous chunks: while the
+# device solves chunk i (the ctypes call releases the GIL, a worker thread waits on it), the host
+# validates and packs chunk i+1 and builds the reports of chunk i-1.  Every scenario's result is
+# bitwise the one of the unchunked launch (same kernel and cluster shape; see tests).
+PIPELINE_MIN_BATCH = 256
+_POOL = None
+_POOL_LOCK = __import__("threading").Lock()
+
+
+def _solver_thread():
+    global _POOL
+    with _POOL_LOCK:
+        if _POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="swarm-solve")
+        return _POOL
+
+
+def _pipeline_chunks(B: int) -> int:
+    env = __import__("os").environ.get("SWARM_PIPE_CHUNKS")
+    if env is not None:
+        return max(1, min(B, int(env)))
+    return 1 if B < PIPELINE_MIN_BATCH else 3
+
+
+def _prep_chunk(specs, basis, n_obs):
+    """Validation (raises before this chunk's device work) and packing of one chunk."""
+    t0 = time.perf_counter()
+    bnd = boundary_arrays(specs)
+    for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0]):
+        if v:
+            raise _infeasible(v)
+    c0, beq, geom = pack(specs, basis, bnd)
+    col_geom = np.array([[sp.geometry.l_xy, sp.geometry.l_z] for sp in specs], dtype=float).reshape(-1, 2)
+    col_obs = (np.stack([metrics._obstacle_rows(sp.geometry, sp.obstacles) for sp in specs]) if n_obs
+               else np.zeros((len(specs), 0, 5)))
+    return t0, time.perf_counter(), c0, beq, geom, col_geom, col_obs
+
+
+def _check_finite(out, offset: int = 0) -> None:
+    bad = np.flatnonzero(out["status"] == native.ST_NONFINITE)
+    if bad.size:
+        raise NonFiniteStateError(
+            f"non-finite pair state (d/beta out of range) in iteration {int(out['iters'][bad[0]])} of scenario "
+            f"{int(bad[0]) + offset}" + (f" and {bad.size - 1} more scenario(s)" if bad.size > 1 else ""))
+
+
+def _am_solve_batch(specs, config, cache, with_metrics) -> list:
     config = config or SolverConfig()
     specs = list(specs)
     if not specs:
@@ -508,40 +585,69 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
     if config.track_descent and len(specs) != 1:
         raise ValueError("track_descent is only available for single solves")
     _check_batch(specs)
-    t0 = time.perf_counter()
-    bnd = boundary_arrays(specs)
-    for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0]):
-        if v:
-            raise _infeasible(v)
     if config.keep_state and len(specs) != 1:
         raise ValueError("keep_state is only available for single solves")
     spec0 = specs[0]
     n, n_obs = len(spec0.start), len(spec0.obstacles)
     basis = poly.for_spec(spec0)
+    report_path = not config.keep_state and basis.num_samples >= 3
+    B = len(specs)
+    K = _pipeline_chunks(B) if report_path else 1
+    bounds = [B * i // K for i in range(K + 1)]
+    prep = _prep_chunk(specs[: bounds[1]], basis, n_obs)
     fp = kkt.fingerprint(basis, n, n_obs)
-    c0, beq, geom = pack(specs, basis, bnd)
-    t1 = time.perf_counter()
     cache, foreign = _resolve_cache(cache)
     schedule = config.schedule()
     before = cache.stats()
     plan = _plan_for(cache, fp, basis, schedule, n, n_obs, _opt(config, "device", 0))
     _sync_foreign(cache, foreign, before)
-    t2 = time.perf_counter()
-    out = plan.solve(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
-                     keep_state=config.keep_state, cluster_hint=_opt(config, "cluster_size", 0),
-                     fp32=_opt(config, "fp32", False))
-    t3 = time.perf_counter()
-    bad = np.flatnonzero(out["status"] == native.ST_NONFINITE)
-    if bad.size:
-        raise NonFiniteStateError(
-            f"non-finite pair state (d/beta out of range) in iteration {int(out['iters'][bad[0]])} of scenario "
-            f"{int(bad[0])}" + (f" and {bad.size - 1} more scenario(s)" if bad.size > 1 else ""))
-    reports = _make_reports(specs, out, basis, plan, cache, schedule, config, (t0, t1, t2, t3), with_metrics,
-                            foreign=foreign)
+    hint, fp32 = _opt(config, "cluster_size", 0), _opt(config, "fp32", False)
+
+    def solve(pr):
+        _, _, c0, beq, geom, col_geom, col_obs = pr
+        t2 = time.perf_counter()
+        if report_path:
+            # one call: solve + trajectories (+ arc length / smoothness, collision summary) on the device
+            out = plan.solve_report(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
+                                    col_geom, col_obs, cluster_hint=hint, fp32=fp32, with_metrics=with_metrics)
+        else:
+            out = plan.solve(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
+                             keep_state=config.keep_state, cluster_hint=hint, fp32=fp32)
+        return out, t2, time.perf_counter()
+
+    def finish(i, pr, res):
+        out, t2, t3 = res
+        _check_finite(out, bounds[i])
+        return _make_reports(specs[bounds[i]: bounds[i + 1]], out, basis, plan, cache, schedule, config,
+                             (pr[0], pr[1], t2, t3), with_metrics, foreign=foreign)
+
+    if K == 1:
+        res = solve(prep)
+        reports = finish(0, prep, res)
+    else:
+        pool = _solver_thread()
+        reports = []
+        fut = pool.submit(solve, prep)
+        for i in range(1, K):
+            try:
+                nxt = _prep_chunk(specs[bounds[i]: bounds[i + 1]], basis, n_obs)
+            except BaseException:
+                fut.result()  # no solve left running on the plan when the error propagates
+                raise
+            res = fut.result()
+            fut = pool.submit(solve, nxt)
+            try:
+                reports += finish(i - 1, prep, res)
+            except BaseException:
+                fut.result()
+                raise
+            prep = nxt
+        reports += finish(K - 1, prep, fut.result())
     if config.track_descent:
+        _, _, c0, beq, geom, _, _ = prep
         reports[0].diagnostics["descent_slack"] = _descent_slack(
             spec0, basis, plan, c0, beq, geom, schedule, config, reports[0].iterations, reports[0].coefficients)
-    log.info("batch of %d solved on device in %.3f ms", len(specs), out["timings_ms"][1])
+    log.info("batch of %d solved on device in %d launch(es)", B, K)
     return reports
 
 

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -24,10 +25,10 @@ ST_FLAG_FP32 = 2
 ST_NONFINITE = -1
 _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedError}
 
-EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_device", "st_query_launch",
+EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_report", "st_solve_device", "st_query_launch",
            "st_last_error", "st_version", "st_shard_layout", "st_shard_buffer", "st_shard_open", "st_shard_close",
            "st_shard_reset", "st_solve_sharded", "st_check_collisions",
-           "st_check_collisions_batch", "st_large_partition")
+           "st_check_collisions_batch", "st_large_partition", "st_host_alloc", "st_host_free")
 
 _lib = None
 _lock = threading.Lock()
@@ -53,6 +54,9 @@ def load() -> ctypes.CDLL:
         lib.st_solve.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip, _dp, _dp,
                                  ctypes.POINTER(ctypes.c_float)]
         lib.st_solve_device.argtypes = [vp, i, vp, vp, vp, i, i, d, i, i, vp, vp, vp, vp, vp, vp, vp]
+        lib.st_solve_report.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip,
+                                        ctypes.POINTER(ctypes.c_float), _dp, _dp, _dp, _dp, _dp, _dp,
+                                        ctypes.POINTER(ctypes.c_longlong)]
         lib.st_query_launch.argtypes = [vp, i, i, i, ctypes.POINTER(ctypes.c_longlong)]
         lib.st_last_error.restype = ctypes.c_char_p
         ub = ctypes.POINTER(ctypes.c_ubyte)
@@ -68,6 +72,8 @@ def load() -> ctypes.CDLL:
         lib.st_check_collisions_batch.argtypes = [i, i, i, _dp, _dp, i, _dp, i, ll, _ip, _dp, _dp,
                                                   ctypes.POINTER(ll)]
         lib.st_large_partition.argtypes = [i, i, i, i, _ip, _ip, _ip, _ip]
+        lib.st_host_alloc.argtypes = [ll, ctypes.POINTER(vp)]
+        lib.st_host_free.argtypes = [vp]
         for name in EXPORTS:
             getattr(lib, name)  # every declared symbol must resolve
         _lib = lib
@@ -85,6 +91,47 @@ def _ptr(a: np.ndarray | None, ctype=_dp):
         return None
     assert a.flags.c_contiguous
     return a.ctypes.data_as(ctype)
+
+
+class _PinnedPool:
+    """Recycled page-locked host buffers for large outputs (report trajectories).
+
+    ``empty(shape)`` returns a float64 array over a pinned buffer; when the array and every
+    view of it are gone, the buffer returns to the pool for the next call of that size
+    (allocating page-locked memory costs far more than the copy it speeds up)."""
+
+    def __init__(self, keep: int = 4):
+        self._free: dict = {}
+        self._lock = threading.Lock()
+        self._keep = keep
+
+    def empty(self, shape) -> np.ndarray:
+        count = int(np.prod(shape))
+        nbytes = max(8, count * 8)
+        with self._lock:
+            bucket = self._free.get(nbytes)
+            ptr = bucket.pop() if bucket else None
+        if ptr is None:
+            p = ctypes.c_void_p()
+            _check(load().st_host_alloc(nbytes, ctypes.byref(p)))
+            ptr = p.value
+        raw = (ctypes.c_byte * nbytes).from_address(ptr)
+        weakref.finalize(raw, self._release, ptr, nbytes)
+        return np.frombuffer(raw, dtype=np.float64, count=count).reshape(shape)
+
+    def _release(self, ptr: int, nbytes: int) -> None:
+        with self._lock:
+            bucket = self._free.setdefault(nbytes, [])
+            if len(bucket) < self._keep:
+                bucket.append(ptr)
+                return
+        try:
+            load().st_host_free(ptr)
+        except Exception:
+            pass
+
+
+_PINNED = _PinnedPool()
 
 
 class Plan:
@@ -166,6 +213,43 @@ class Plan:
                                   _ptr(hist), _ptr(iters, _ip), _ptr(conv, _ip), _ptr(lam), _ptr(d), t))
         return {"c": c_out, "hist": hist, "iters": iters, "converged": conv if out is not None else conv > 0,
                 "status": conv.copy(), "lam": lam, "d": d, "timings_ms": tuple(float(x) for x in t)}
+
+    def solve_report(self, c0, beq, geom, switch_every: int, max_iters: int, tol: float, col_geom, col_obs,
+                     cluster_hint: int = 0, fp32: bool = False, with_metrics: bool = True) -> dict:
+        """``solve`` plus the report's post-loop work on the device in the same call
+        (``st_solve_report``): trajectories (B, n, m, 3), arc length and smoothness (B, n),
+        and the collision summary -- minimum normalized distance and violation count (B,) --
+        from ``col_geom`` (B, 2) and ``col_obs`` (B, n_obs, 5) as for the collision check."""
+        c0 = np.ascontiguousarray(c0, dtype=np.float64)
+        beq = np.ascontiguousarray(beq, dtype=np.float64)
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        col_geom = np.ascontiguousarray(col_geom, dtype=np.float64)
+        col_obs = np.ascontiguousarray(col_obs, dtype=np.float64)
+        B = c0.shape[0]
+        if c0.shape != (B, 3, self.n, self.nv) or beq.shape != (B, 3, self.n, 6) or \
+                geom.shape != (B, 2 + 5 * self.n_obs) or col_geom.shape != (B, 2) or \
+                col_obs.shape != (B, self.n_obs, 5):
+            raise ValueError("batch arrays do not match the plan's shape")
+        c_out = np.empty_like(c0)
+        hist = np.empty((B, 3, max_iters))
+        iters = np.empty(B, dtype=np.int32)
+        conv = np.empty(B, dtype=np.int32)
+        traj = _PINNED.empty((B, self.n, self.m, 3))
+        arc = np.empty((B, self.n)) if with_metrics else None
+        smooth = np.empty((B, self.n)) if with_metrics else None
+        mind = np.empty(B) if with_metrics else None
+        nviol = np.empty(B, dtype=np.int64) if with_metrics else None
+        t = (ctypes.c_float * 3)()
+        _check(self._lib.st_solve_report(self._h, B, _ptr(c0), _ptr(beq), _ptr(geom), switch_every, max_iters, tol,
+                                         ST_FLAG_FP32 if fp32 else 0, cluster_hint, _ptr(c_out), _ptr(hist),
+                                         _ptr(iters, _ip), _ptr(conv, _ip), t, _ptr(col_geom), _ptr(col_obs),
+                                         _ptr(traj), _ptr(arc), _ptr(smooth), _ptr(mind),
+                                         _ptr(nviol, ctypes.POINTER(ctypes.c_longlong))))
+        res = {"c": c_out, "hist": hist, "iters": iters, "converged": conv > 0, "status": conv, "lam": None,
+               "d": None, "timings_ms": tuple(float(x) for x in t), "traj": traj}
+        if with_metrics:
+            res.update(arc=arc, smooth=smooth, min_dist=mind, n_viol=nviol)
+        return res
 
     def solve_device(self, B: int, c0_ptr: int, beq_ptr: int, geom_ptr: int, switch_every: int,
                      max_iters: int, tol: float, c_out_ptr: int, hist_ptr: int, iters_ptr: int,

@@ -1,5 +1,5 @@
-"""Whole-call throughput of am_solve_batch (validation, packing, device loop, reports with the
-batched device collision verdict) for 1024 rand32 scenarios."""
+"""Whole-call throughput of am_solve_batch (validation, packing, device loop + device report
+pass, reports) for 1024 rand32 scenarios, by pipeline chunk count; optional cProfile."""
 import os
 import sys
 import time
@@ -10,14 +10,19 @@ from paper_2011_04240_b200 import FactorCache, am_solve_batch, generate_random  
 specs = [generate_random(32, (8, 8, 3), 0.4, s) for s in range(1024)]
 cache = FactorCache()
 am_solve_batch(specs, cache=cache)
-for with_metrics in (False, True):
-    t = time.perf_counter()
-    reps = am_solve_batch(specs, cache=cache, with_metrics=with_metrics)
-    wall = time.perf_counter() - t
-    print(f"am_solve_batch(1024 rand32, with_metrics={with_metrics}): {wall * 1e3:.1f} ms -> "
-          f"{1024 / wall:.0f} solves/s (device loop {reps[0].timings['loop_s'] * 1e3:.1f} ms)", flush=True)
+for chunks in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["1", "2", "3", "4"]):
+    os.environ["SWARM_PIPE_CHUNKS"] = chunks
+    for with_metrics in (False, True):
+        best = 1e9
+        for _ in range(3):
+            t = time.perf_counter()
+            reps = am_solve_batch(specs, cache=cache, with_metrics=with_metrics)
+            best = min(best, time.perf_counter() - t)
+        print(f"am_solve_batch(1024 rand32, with_metrics={with_metrics}, chunks={chunks}): {best * 1e3:.1f} ms -> "
+              f"{1024 / best:.0f} solves/s (device loop of one launch {reps[0].timings['loop_s'] * 1e3:.1f} ms)",
+              flush=True)
 
-if len(sys.argv) > 1:
+if len(sys.argv) > 2:
     import cProfile
     import pstats
     pr = cProfile.Profile()

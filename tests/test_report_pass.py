@@ -1,0 +1,89 @@
+"""The device report pass (``st_solve_report``) and the pipelined batch entry.
+
+``am_solve_batch`` forms the reports' trajectories, arc length / smoothness and the
+collision summary on the device in the solve call (replacing the host work after the
+reference's loop: SolveReport.trajectories = c_axis @ P.T, solver.py:133-136, and
+_final_metrics, solver.py:497-509 -> validation.py:39-132), and runs large batches as a
+pipeline of chunks.  Checked here against the host formulas on the same coefficients, the
+scalar collision loop, and the unchunked launch (bitwise).
+"""
+
+import numpy as np
+import pytest
+
+
+def _specs(B, n=32, seed0=0, obstacles=0):
+    from paper_2011_04240_b200 import generate_random, generate_random_with_obstacles
+    if obstacles:
+        return [generate_random_with_obstacles(n, (8.0, 8.0, 3.0), 0.4, obstacles, 0.5, seed=seed0 + s)
+                for s in range(B)]
+    return [generate_random(n, (8, 8, 3), 0.4, seed0 + s) for s in range(B)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("obstacles", [0, 4])
+def test_report_pass_matches_host_formulas(cuda_ok, obstacles):
+    from paper_2011_04240_b200 import am_solve_batch, metrics, poly
+    specs = _specs(40, n=12 if obstacles else 32, obstacles=obstacles)
+    reps = am_solve_batch(specs)
+    basis = poly.for_spec(specs[0])
+    for spec, r in zip(specs, reps):
+        host_traj = np.stack([r.coefficients[a] @ basis.P.T for a in range(3)], axis=-1)
+        np.testing.assert_allclose(r.trajectories, host_traj, rtol=1e-13, atol=1e-13)
+        q = metrics.trajectory_metrics(host_traj)
+        np.testing.assert_allclose(r.metrics["arc_length"], q.arc_length, rtol=1e-12)
+        np.testing.assert_allclose(r.metrics["smoothness"], q.smoothness, rtol=1e-12)
+        assert r.metrics["mean_arc_length"] == pytest.approx(np.mean(q.arc_length), rel=1e-12)
+        # verdict on the report's own trajectories: identical to the scalar loop of the reference
+        col = metrics.check_collisions(r.trajectories, spec.geometry, spec.obstacles)
+        assert r.metrics["num_collision_violations"] == len(col.violations)
+        md = r.metrics["min_normalized_distance"]
+        assert (md is None) == np.isinf(col.min_normalized_distance)
+        if md is not None:
+            assert md == col.min_normalized_distance
+
+
+@pytest.mark.gpu
+def test_pipelined_batch_is_bitwise_the_single_launch(cuda_ok, monkeypatch):
+    from paper_2011_04240_b200 import am_solve_batch
+    specs = _specs(300)
+    monkeypatch.setenv("SWARM_PIPE_CHUNKS", "1")
+    one = am_solve_batch(specs)
+    monkeypatch.setenv("SWARM_PIPE_CHUNKS", "3")
+    three = am_solve_batch(specs)
+    monkeypatch.setenv("SWARM_PIPE_CHUNKS", "7")
+    seven = am_solve_batch(specs, with_metrics=False)
+    assert {r.timings["batch"] for r in three} == {100}
+    for a, b, c in zip(one, three, seven):
+        assert a.iterations == b.iterations == c.iterations
+        assert np.array_equal(a.coefficients, b.coefficients) and np.array_equal(a.coefficients, c.coefficients)
+        assert np.array_equal(a.trajectories, b.trajectories) and np.array_equal(a.trajectories, c.trajectories)
+        assert a.residual_norm_history == b.residual_norm_history
+        assert a.metrics == b.metrics
+        assert c.metrics == {}
+
+
+@pytest.mark.gpu
+def test_pipelined_batch_raises_on_a_late_invalid_scenario(cuda_ok, monkeypatch):
+    from paper_2011_04240_b200 import InfeasibleProblemError, am_solve_batch
+    specs = _specs(300)
+    bad = specs[250]
+    # two agents at the same start: infeasible (reference problem.py:162-194)
+    start = (bad.start[1],) + tuple(bad.start[1:])
+    specs[250] = type(bad)(start=start, goal=bad.goal, geometry=bad.geometry, obstacles=bad.obstacles,
+                           num_samples=bad.num_samples, degree=bad.degree, duration=bad.duration,
+                           basis_kind=bad.basis_kind, seed=bad.seed)
+    monkeypatch.setenv("SWARM_PIPE_CHUNKS", "3")
+    with pytest.raises(InfeasibleProblemError):
+        am_solve_batch(specs)
+    # the plan is left usable
+    assert am_solve_batch(specs[:5])[0].converged
+
+
+def test_pipeline_chunking_rule(monkeypatch):
+    from paper_2011_04240_b200 import engine
+    monkeypatch.delenv("SWARM_PIPE_CHUNKS", raising=False)
+    assert engine._pipeline_chunks(1) == 1 and engine._pipeline_chunks(255) == 1
+    assert engine._pipeline_chunks(1024) == 3
+    monkeypatch.setenv("SWARM_PIPE_CHUNKS", "5")
+    assert engine._pipeline_chunks(3) == 3 and engine._pipeline_chunks(100) == 5
