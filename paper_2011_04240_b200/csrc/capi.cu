@@ -190,7 +190,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   k.xch_norm = 3 * NV;
   k.rx = k.red ? (int)rx : 0;
   take(k.o_X, (long long)L.tasks_max * k.xs);
-  take(k.o_tab, (L.tmax + 1) / 2);
+  take(k.o_tab, (L.tmax + 1) / 2);  // per-time warp ranges
   take(k.o_P, (long long)k.prow * NV);
   take(k.o_cown, k.red ? 0 : (long long)L.own_max * 3 * NV);
   take(k.o_nrm, 3LL * C);

@@ -590,7 +590,7 @@ def _am_solve_batch(specs, config, cache, with_metrics) -> list:
     spec0 = specs[0]
     n, n_obs = len(spec0.start), len(spec0.obstacles)
     basis = poly.for_spec(spec0)
-    report_path = not config.keep_state and basis.num_samples >= 3
+    report_path = not config.keep_state and basis.num_samples >= 3 and native.load().swarm_has_report
     B = len(specs)
     K = _pipeline_chunks(B) if report_path else 1
     bounds = [B * i // K for i in range(K + 1)]

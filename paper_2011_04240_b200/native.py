@@ -54,9 +54,14 @@ def load() -> ctypes.CDLL:
         lib.st_solve.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip, _dp, _dp,
                                  ctypes.POINTER(ctypes.c_float)]
         lib.st_solve_device.argtypes = [vp, i, vp, vp, vp, i, i, d, i, i, vp, vp, vp, vp, vp, vp, vp]
-        lib.st_solve_report.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip,
-                                        ctypes.POINTER(ctypes.c_float), _dp, _dp, _dp, _dp, _dp, _dp,
-                                        ctypes.POINTER(ctypes.c_longlong)]
+        optional = set()
+        if os.environ.get("SWARM_LIB"):
+            # A/B runs against an older build of the library: entries it lacks are optional
+            optional = {nm for nm in ("st_solve_report", "st_host_alloc", "st_host_free") if not hasattr(lib, nm)}
+        if "st_solve_report" not in optional:
+            lib.st_solve_report.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip,
+                                            ctypes.POINTER(ctypes.c_float), _dp, _dp, _dp, _dp, _dp, _dp,
+                                            ctypes.POINTER(ctypes.c_longlong)]
         lib.st_query_launch.argtypes = [vp, i, i, i, ctypes.POINTER(ctypes.c_longlong)]
         lib.st_last_error.restype = ctypes.c_char_p
         ub = ctypes.POINTER(ctypes.c_ubyte)
@@ -72,10 +77,13 @@ def load() -> ctypes.CDLL:
         lib.st_check_collisions_batch.argtypes = [i, i, i, _dp, _dp, i, _dp, i, ll, _ip, _dp, _dp,
                                                   ctypes.POINTER(ll)]
         lib.st_large_partition.argtypes = [i, i, i, i, _ip, _ip, _ip, _ip]
-        lib.st_host_alloc.argtypes = [ll, ctypes.POINTER(vp)]
-        lib.st_host_free.argtypes = [vp]
+        if "st_host_alloc" not in optional:
+            lib.st_host_alloc.argtypes = [ll, ctypes.POINTER(vp)]
+            lib.st_host_free.argtypes = [vp]
         for name in EXPORTS:
-            getattr(lib, name)  # every declared symbol must resolve
+            if name not in optional:
+                getattr(lib, name)  # every declared symbol must resolve
+        lib.swarm_has_report = "st_solve_report" not in optional
         _lib = lib
         return lib
 
