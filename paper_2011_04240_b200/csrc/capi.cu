@@ -110,6 +110,8 @@ struct st_plan {
   void* d_rg = nullptr;
   size_t rg_bytes = 0;
   void* d_io = nullptr;  // inputs+outputs of host-pointer solves
+  void* h_stage = nullptr;  // page-locked staging of small host-pointer solves (one H2D, one D2H)
+  size_t stage_bytes = 0;
   size_t io_bytes = 0;
   int smem_optin = 0;
   int smem_sm = 0;  // shared memory per SM
@@ -685,8 +687,11 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       at[na].id = cudaLaunchAttributeAccessPolicyWindow;
       at[na].val.accessPolicyWindow.base_ptr = pl->d_lam;
       at[na].val.accessPolicyWindow.num_bytes = std::min(used, (size_t)max_window);
-      at[na].val.accessPolicyWindow.hitRatio =
-          (float)std::min(1.0, (double)max_persist / std::max(1.0, gfrac * at[na].val.accessPolicyWindow.num_bytes));
+      // persisting lines at 80% of the set-aside: a cyclic stream that just overfills it thrashes
+      // the LRU (1024 rand32, 87 MB window, 79 MB touched vs 83 MB set-aside: hit ratio 1.0 ->
+      // 31 GB DRAM per launch, 0.85 -> 19 GB and 1.4% faster; profiles/l2_hit_sweep_r2.txt)
+      at[na].val.accessPolicyWindow.hitRatio = (float)std::min(
+          1.0, 0.8 * (double)max_persist / std::max(1.0, gfrac * at[na].val.accessPolicyWindow.num_bytes));
       if (const char* hr = std::getenv("SWARM_L2_HIT")) at[na].val.accessPolicyWindow.hitRatio = (float)std::atof(hr);
       at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
@@ -1083,6 +1088,7 @@ int st_plan_destroy(st_plan* pl) {
   if (pl->d_cws) cudaFree(pl->d_cws);
   if (pl->d_rg) cudaFree(pl->d_rg);
   if (pl->d_io) cudaFree(pl->d_io);
+  if (pl->h_stage) cudaFreeHost(pl->h_stage);
   if (pl->d_lgw) cudaFree(pl->d_lgw);
   if (pl->d_rep) cudaFree(pl->d_rep);
   if (pl->stream) cudaStreamDestroy(pl->stream);
@@ -1159,10 +1165,29 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   int* d_it = (int*)(d_dd + n_d);
   int* d_cv = d_it + batch;
   cudaStream_t s = pl->stream;
+  // small solves (single scenarios): inputs and the small outputs go through one page-locked
+  // staging buffer -- one H2D and one D2H instead of a pageable copy per array
+  const size_t small_out = (n_c + n_h) * 8 + 2 * (size_t)batch * 4 + (rep ? (size_t)batch * (2 * n + 2) * 8 : 0);
+  const bool staged = !keep && in_bytes + small_out <= ((size_t)1 << 20);
+  if (staged && in_bytes + small_out > pl->stage_bytes) {
+    if (pl->h_stage) cudaFreeHost(pl->h_stage);
+    pl->h_stage = nullptr;
+    pl->stage_bytes = 0;
+    ST_CUDA(cudaHostAlloc(&pl->h_stage, (size_t)1 << 20, cudaHostAllocPortable));
+    pl->stage_bytes = (size_t)1 << 20;
+  }
+  double* hs = staged ? (double*)pl->h_stage : nullptr;
   ST_CUDA(cudaEventRecord(pl->ev[0], s));
-  ST_CUDA(cudaMemcpyAsync(d_c0, c0, n_c * 8, cudaMemcpyHostToDevice, s));
-  ST_CUDA(cudaMemcpyAsync(d_beq, beq, n_b * 8, cudaMemcpyHostToDevice, s));
-  ST_CUDA(cudaMemcpyAsync(d_geom, geom, n_g * 8, cudaMemcpyHostToDevice, s));
+  if (staged) {
+    memcpy(hs, c0, n_c * 8);
+    memcpy(hs + n_c, beq, n_b * 8);
+    memcpy(hs + n_c + n_b, geom, n_g * 8);
+    ST_CUDA(cudaMemcpyAsync(d_c0, hs, in_bytes, cudaMemcpyHostToDevice, s));
+  } else {
+    ST_CUDA(cudaMemcpyAsync(d_c0, c0, n_c * 8, cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_beq, beq, n_b * 8, cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_geom, geom, n_g * 8, cudaMemcpyHostToDevice, s));
+  }
   ST_CUDA(cudaEventRecord(pl->ev[1], s));
   rc = large ? run_large(pl, (flags & ST_FLAG_FP32) != 0, d_c0, d_beq, d_geom, switch_every, max_iters, tol, d_cout,
                          d_hist, d_it, d_cv, s, ext)
@@ -1171,6 +1196,7 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   if (rc) return rc;
   ST_CUDA(cudaEventRecord(pl->ev[2], s));
   std::vector<unsigned long long> mt;
+  const double* rep_small = nullptr;  // device: arc | smooth | min bits | counts (report pass)
   if (rep) {
     // report pass on the device: trajectories, arc length / smoothness, collision summary
     const int n_obs = pl->nobs;
@@ -1179,7 +1205,9 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     const size_t b_traj = al((size_t)batch * n * m * 24), b_met = al((size_t)batch * n * 16),
                  b_geom = al((size_t)batch * 16), b_obs = al((size_t)batch * n_obs * 40 + 8),
                  b_cnt = al((size_t)batch * n_rows * 4 + 4), b_mt = al((size_t)batch * 16);
-    const size_t rneed = b_traj + b_met + b_geom + b_obs + b_cnt + b_mt;
+    (void)b_met;
+    const size_t b_small = al((size_t)batch * (2 * n + 2) * 8);  // arc | smooth | min bits | counts
+    const size_t rneed = b_traj + b_small + b_geom + b_obs + b_cnt;
     if (rneed > pl->rep_bytes) {
       if (pl->d_rep) cudaFree(pl->d_rep);
       pl->d_rep = nullptr;
@@ -1191,10 +1219,11 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     double* r_traj = (double*)q;
     double* r_arc = (double*)(q += b_traj);
     double* r_smooth = r_arc + (size_t)batch * n;
-    double* r_geom = (double*)(q += b_met);
+    unsigned long long* r_mt = (unsigned long long*)(r_smooth + (size_t)batch * n);
+    double* r_geom = (double*)(q += b_small);
     double* r_obs = (double*)(q += b_geom);
     int* r_cnt = (int*)(q += b_obs);
-    unsigned long long* r_mt = (unsigned long long*)(q += b_cnt);
+    rep_small = r_arc;
     const bool verdict = rep->min_dist || rep->n_viol;
     if (verdict) {
       ST_CUDA(cudaMemcpyAsync(r_geom, rep->geom2, (size_t)batch * 16, cudaMemcpyHostToDevice, s));
@@ -1204,16 +1233,27 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     if (verdict) {
       ST_CUDA(swarm_collision_summary_launch(batch, n, m, r_traj, r_geom, n_obs, r_obs, r_cnt, r_mt, s));
       mt.resize(2 * (size_t)batch);
-      ST_CUDA(cudaMemcpyAsync(mt.data(), r_mt, (size_t)batch * 16, cudaMemcpyDeviceToHost, s));
+      if (!staged) ST_CUDA(cudaMemcpyAsync(mt.data(), r_mt, (size_t)batch * 16, cudaMemcpyDeviceToHost, s));
     }
     if (rep->traj) ST_CUDA(cudaMemcpyAsync(rep->traj, r_traj, (size_t)batch * n * m * 24, cudaMemcpyDeviceToHost, s));
-    if (rep->arc) ST_CUDA(cudaMemcpyAsync(rep->arc, r_arc, (size_t)batch * n * 8, cudaMemcpyDeviceToHost, s));
-    if (rep->smooth) ST_CUDA(cudaMemcpyAsync(rep->smooth, r_smooth, (size_t)batch * n * 8, cudaMemcpyDeviceToHost, s));
+    if (!staged) {
+      if (rep->arc) ST_CUDA(cudaMemcpyAsync(rep->arc, r_arc, (size_t)batch * n * 8, cudaMemcpyDeviceToHost, s));
+      if (rep->smooth)
+        ST_CUDA(cudaMemcpyAsync(rep->smooth, r_smooth, (size_t)batch * n * 8, cudaMemcpyDeviceToHost, s));
+    }
   }
-  ST_CUDA(cudaMemcpyAsync(c_out, d_cout, n_c * 8, cudaMemcpyDeviceToHost, s));
-  ST_CUDA(cudaMemcpyAsync(hist, d_hist, n_h * 8, cudaMemcpyDeviceToHost, s));
-  ST_CUDA(cudaMemcpyAsync(iters, d_it, batch * 4, cudaMemcpyDeviceToHost, s));
-  ST_CUDA(cudaMemcpyAsync(conv, d_cv, batch * 4, cudaMemcpyDeviceToHost, s));
+  // output region of d_io: c | hist | (lam | d) | iters | converged
+  const size_t out_small = (n_c + n_h) * 8 + 2 * (size_t)batch * 4;
+  if (staged) {
+    ST_CUDA(cudaMemcpyAsync(hs, d_cout, out_small, cudaMemcpyDeviceToHost, s));
+    if (rep) ST_CUDA(cudaMemcpyAsync((char*)hs + out_small, rep_small, (size_t)batch * (2 * n + 2) * 8,
+                                     cudaMemcpyDeviceToHost, s));
+  } else {
+    ST_CUDA(cudaMemcpyAsync(c_out, d_cout, n_c * 8, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(hist, d_hist, n_h * 8, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(iters, d_it, batch * 4, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(conv, d_cv, batch * 4, cudaMemcpyDeviceToHost, s));
+  }
   if (keep) {
     ST_CUDA(cudaMemcpyAsync(lam_out, d_lam, n_lam * 8, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaMemcpyAsync(d_out, d_dd, n_d * 8, cudaMemcpyDeviceToHost, s));
@@ -1225,6 +1265,19 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     ST_CUDA(cudaEventElapsedTime(&timings[0], pl->ev[0], pl->ev[1]));
     ST_CUDA(cudaEventElapsedTime(&timings[1], pl->ev[1], pl->ev[2]));
     ST_CUDA(cudaEventElapsedTime(&timings[2], pl->ev[2], pl->ev[3]));
+  }
+  if (staged) {
+    const char* o = (const char*)hs;
+    memcpy(c_out, o, n_c * 8);
+    memcpy(hist, o + n_c * 8, n_h * 8);
+    memcpy(iters, o + (n_c + n_h) * 8, (size_t)batch * 4);
+    memcpy(conv, o + (n_c + n_h) * 8 + (size_t)batch * 4, (size_t)batch * 4);
+    if (rep) {
+      const char* r = o + out_small;
+      if (rep->arc) memcpy(rep->arc, r, (size_t)batch * n * 8);
+      if (rep->smooth) memcpy(rep->smooth, r + (size_t)batch * n * 8, (size_t)batch * n * 8);
+      if (!mt.empty()) memcpy(mt.data(), r + (size_t)batch * 2 * n * 8, (size_t)batch * 16);
+    }
   }
   if (rep && !mt.empty()) {
     for (int b = 0; b < batch; ++b) {

@@ -559,9 +559,14 @@ def _prep_chunk(specs, basis, n_obs):
     """Validation (raises before this chunk's device work) and packing of one chunk."""
     t0 = time.perf_counter()
     bnd = boundary_arrays(specs)
-    for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0]):
+    if len(specs) == 1:  # the per-spec check: no batch-vectorization overhead for single solves
+        v = validate(specs[0])
         if v:
             raise _infeasible(v)
+    else:
+        for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0]):
+            if v:
+                raise _infeasible(v)
     c0, beq, geom = pack(specs, basis, bnd)
     col_geom = np.array([[sp.geometry.l_xy, sp.geometry.l_z] for sp in specs], dtype=float).reshape(-1, 2)
     col_obs = (np.stack([metrics._obstacle_rows(sp.geometry, sp.obstacles) for sp in specs]) if n_obs

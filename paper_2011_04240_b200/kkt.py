@@ -94,9 +94,18 @@ class Fingerprint:
     basis_sha: str
 
     def key(self) -> str:
-        text = (f"{self.num_agents},{self.num_samples},{self.num_coeffs},{self.num_obstacles},"
-                f"{self.basis_kind},{self.basis_sha}")
-        return hashlib.sha256(text.encode()).hexdigest()[:16]
+        k = _KEYS.get(self)
+        if k is None:
+            text = (f"{self.num_agents},{self.num_samples},{self.num_coeffs},{self.num_obstacles},"
+                    f"{self.basis_kind},{self.basis_sha}")
+            k = hashlib.sha256(text.encode()).hexdigest()[:16]
+            if len(_KEYS) > 256:
+                _KEYS.clear()
+            _KEYS[self] = k
+        return k
+
+
+_KEYS: dict = {}  # Fingerprint -> key (the digest text is fixed per fingerprint)
 
 
 _DIGESTS: dict = {}
@@ -229,6 +238,13 @@ class FactorCache:
                 self._inflight.pop(key).set()
 
     def prefactorize(self, fp: Fingerprint, basis: poly.Basis, schedule: RhoSchedule) -> list:
+        # warm path: every stage present -> one lock, the same hits as one get() per stage
+        fk = fp.key()
+        with self._lock:
+            ops = [self._ops.get((fk, float(rho))) for rho in schedule.values]
+            if all(op is not None for op in ops):
+                self.hits += len(ops)
+                return ops
         return [self.get(fp, basis, rho) for rho in schedule.values]
 
     # -- disk persistence (kkt_cache.py:458-528) ---------------------------------------------------
