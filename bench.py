@@ -20,7 +20,8 @@ whole batch (every scenario to convergence or max_iters) in one device launch.
 * ``fp32``: the same batch in the optional FP32 mode, device time.
 * ``python_api``: the same batch through the Python drop-in ``am_solve_batch`` (Python spec
   objects in, SolveReports with metrics out), whole call.
-* ``single_solve_ms``: BASELINE's "ms per joint solve at 16/32/64/256 agents" -- circ16j,
+* ``single_solve_ms``: BASELINE's "ms per joint solve at 16/32/64/256 agents" -- circ16j, hall16j (the
+  reference CLI's default corridor: 16 agents, 22 wall obstacles),
   rand32_s0, sph64j, rand128_s0, rand256_s0: device loop (best of 3), whole am_solve call,
   FP32 mode, the same-run CPU reference (oracle port, 1 thread; a bounded prefix for
   n > 64) and the loop's roofline fraction.
@@ -236,7 +237,7 @@ def _pair_samples(spec, iters: int) -> float:
     return float((n * (n - 1) // 2 + n * len(spec.obstacles)) * m * (iters + 1))
 
 
-def single_solve_ms(names=("circ16j", "rand32_s0", "sph64j", "rand128_s0", "rand256_s0"), cpu=True,
+def single_solve_ms(names=("circ16j", "rand32_s0", "hall16j", "sph64j", "rand128_s0", "rand256_s0"), cpu=True,
                     fp64_peak=37.2, hbm_peak=6447.8):
     """BASELINE metric "ms per joint solve at 16/32/64/256 agents": device loop (best of 3),
     whole am_solve call, FP32 mode, the same-run CPU reference, and the roofline fraction of

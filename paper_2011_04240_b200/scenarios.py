@@ -218,7 +218,17 @@ def sphere_swap(n=64, radius=0.4, sphere_radius=4.0, z0=4.0, jitter_amp=0.05, se
 
 
 def named(name: str) -> ProblemSpec:
-    """The SURVEY.md §8(d) configs by name: circ16j, circ16, sph16j, sph64j, rand32_s<k>, rand256_s<k>."""
+    """The SURVEY.md §8(d) configs by name: circ16j, circ16, sph16j, sph64j, rand32_s<k>, rand256_s<k>,
+    and hall<n>[j]: the reference CLI/service's default corridor (generate_hallway(n, 20, 4, 0.4),
+    cli.py:80-83) -- the obstacle-heavy case (two walls of sphere obstacles); "j" jitters the
+    boundary positions as for the swaps (the exact corridor is symmetric and chaotic)."""
+    if name.startswith("hall"):
+        spec = generate_hallway(int(name[4:].rstrip("j")), 20.0, 4.0, 0.4)
+        if name.endswith("j"):
+            js, jg = jitter([s.position for s in spec.start], [g.position for g in spec.goal], 0.05, 0)
+            spec = replace(spec, start=tuple(BoundaryState.at_rest(p) for p in js),
+                           goal=tuple(BoundaryState.at_rest(p) for p in jg))
+        return spec
     if name.startswith("circ"):
         n = int(name[4:].rstrip("j"))
         return circle_swap(n, jitter_amp=0.05 if name.endswith("j") else 0.0)

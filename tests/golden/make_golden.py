@@ -115,6 +115,9 @@ def scenarios(st):
         "rand32_s1": (P.generate_random(32, (8, 8, 3), 0.4, 1), {}, False),
         "obs8": (P.generate_random_with_obstacles(8, (8, 8, 3), 0.4, 4, 0.5, 1), {}, False),
         "hallway4j": (jit(hall), {}, False),
+        # the reference CLI/service default corridor (cli.py:80-83): 16 agents, 22 wall obstacles,
+        # symmetry broken like the swaps (the exact corridor is chaotic: envelope 0.6)
+        "hall16j": (jit(P.generate_hallway(16, 20.0, 4.0, 0.4)), {}, False),
         "square4_monomial": (dataclasses.replace(P.generate_square(4, 8.0, 0.4, num_samples=50),
                                                  basis_kind=st.BasisKind.MONOMIAL, degree=6), {}, False),
         "rand48_s0": (P.generate_random(48, (10, 10, 4), 0.4, 0), {}, False),
