@@ -156,7 +156,8 @@ long long layout(st_plan* pl, Launch& L, int C) {
   // redundant solve (every CTA solves all agents, one cluster barrier per iteration) for small
   // single-cluster launches; wide clusters and multi-cluster launches use owners + all-gather
   const char* re = std::getenv("SWARM_RED");
-  k.red = (L.G * L.K == 1 && !L.c_global && C <= 4 && (!re || std::atoi(re) != 0)) ? 1 : 0;
+  const int red_max = re ? std::atoi(re) : 4;  // SWARM_RED=0 disables, =C allows clusters up to C CTAs
+  k.red = (L.G * L.K == 1 && !L.c_global && C <= red_max) ? 1 : 0;
   L.own_max = k.red ? n : ceil_div(n, C);
   const int NV = L.NVMAX;
   const bool obst = pl->nobs > 0;
