@@ -493,69 +493,23 @@ __device__ __forceinline__ void lg_norms(const double* slots, int count, double&
   mx = b;
 }
 
-// c_j = rho G R_j + F (beq_j - beqbar) + Fm beqbar (kkt.py, no obstacles: Rbar = 0), the
-// boundary rows E c_j - beq_j (solver.py:448-452; order-free max), then the coefficients and
-// positions X[t][ax][j] = P[t,:] c_j.  R (all lanes) -> c (all lanes).
-template <int NVMAX>
-__device__ __forceinline__ void lg_solve_row(const LgParams& p, const LgCtx& cx, const double* mat,
-                                             const double* bbar, const double* Ps, int k, int ax, int j,
-                                             double (&c)[NVMAX], bool solve) {
-  using SM = StageMats<NVMAX>;
-  const int lane = threadIdx.x & 31;
-  const int n = p.n;
-  if (solve) {
-    const double rho = mat[SM::RHO];
-    const double* bj = p.beq + ((long long)ax * n + j) * 6;
-    // lane q < NVMAX: output q; then every lane receives all of c
-    const int q = lane < NVMAX ? lane : 0;
-    double s1 = 0.0, s3 = 0.0, s4 = 0.0;
-#pragma unroll
-    for (int i = 0; i < NVMAX; ++i) s1 = fma(mat[SM::G + q * NVMAX + i], c[i], s1);
-#pragma unroll
-    for (int e = 0; e < 6; ++e) {
-      const double bm = bbar[ax * 6 + e];
-      s3 = fma(mat[SM::F + q * 6 + e], __ldg(bj + e) - bm, s3);
-      s4 = fma(mat[SM::Fm + q * 6 + e], bm, s4);
-    }
-    const double out = rho * s1 + (s3 + s4);
-#pragma unroll
-    for (int i = 0; i < NVMAX; ++i) c[i] = __shfl_sync(0xffffffffu, out, i);
-    double bmx = 0.0;
-    if (lane < 6) {
-      double v = 0.0;
-#pragma unroll
-      for (int i = 0; i < NVMAX; ++i) v = fma(p.E[lane * NVMAX + i], c[i], v);
-      bmx = fabs(v - __ldg(bj + lane));
-    }
-    bmx = warp_max(bmx);
-    if (lane == 0 && bmx > 0.0) atomicMax(cx.bnd + (k % 3), (unsigned long long)__double_as_longlong(bmx));
-  }
-  if (lane < NVMAX) {
-    double v = 0.0;
-#pragma unroll
-    for (int q = 0; q < NVMAX; ++q) v = (q == lane) ? c[q] : v;
-    cx.cbuf[((long long)ax * n + j) * NVMAX + lane] = v;
-  }
-  for (int t = lane; t < p.m; t += 32) {
-    const double* pr = Ps + t * NVMAX;
-    double v = 0.0;
-#pragma unroll
-    for (int q = 0; q < NVMAX; ++q) v = fma(pr[q], c[q], v);
-    cx.X[((long long)t * 3 + ax) * p.npad + j] = v;
-  }
-}
-
 // R phase: CTA c of the group owns the rows r = ax * n + j in [c R / cpg, (c+1) R / cpg),
 // R = 3n.  mode 0: initial positions from c0; mode 1: reduce the group's unit slots and solve
 // (G == 1); mode 2: reduce and publish the partial row (G > 1); mode 3: sum the G published
-// partials in rank order and solve (G > 1, after the exchange).
-// The reduction runs in two steps so that every thread of the CTA has its slot loads in flight
-// at once: (1) thread = (row, t): q_j(t) = sum of the row's unit slots at t, block pairs in
-// ascending order, into shared memory (the multiplier ring is idle in this phase); (2) warp =
-// row: R_j = sum_t q_j(t) P[t,:] (t by lane, then a butterfly, bitwise identical on all lanes).
+// partials in rank order and solve (G > 1, after the exchange).  Every step uses the whole CTA:
+//   1. thread = (row, t): q_j(t) = sum of the row's unit slots at t, block pairs ascending, into
+//      shared memory (all slot loads in flight at once; the multiplier ring is idle here);
+//   2. R (rows x NVMAX) = q (rows x m) P (m x NVMAX) as FP64 tensor-core tiles (DMMA), the k
+//      steps (samples) split over the warps, the warp partials added in warp order;
+//   3. thread = (row, coefficient): c_j = rho G R_j + F (beq_j - beqbar) + Fm beqbar (kkt.py, no
+//      obstacles: Rbar = 0); then thread = (row, endpoint row): |E c_j - beq_j| (order-free max);
+//   4. thread = (row, t): positions X[t][ax][j] = P[t,:] c_j (k-ascending FMA chain).
+// A fixed order everywhere: bitwise reproducible, and identical on every GPU of a sharded solve.
 template <int NVMAX>
 __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsigned char* smb, const LgSmem& L, int k,
                                         int mode, long long* tsr = nullptr) {
+  using SM = StageMats<NVMAX>;
+  constexpr int NH = (NVMAX + 7) / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* Ps = reinterpret_cast<const double*>(smb + L.P);
   const double* mat = reinterpret_cast<const double*>(smb + L.mat);
@@ -564,83 +518,149 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
   const int n = p.n, m = p.m, R3 = 3 * n;
   const int r_lo = (int)((long long)cx.cta * R3 / p.cpg), r_hi = (int)((long long)(cx.cta + 1) * R3 / p.cpg);
   const int nr = r_hi - r_lo;
+  const int mt_n = (nr + 7) >> 3, rp = mt_n * 8;  // row tiles of the projection
   const long long xstride = 3LL * n * NVMAX + 4;
-  double* qs = reinterpret_cast<double*>(smb + L.ring);  // nr x m, reusing the multiplier ring
+  // scratch in the multiplier ring (idle in this phase): q rows | warp partials | R | c
+  double* qs = reinterpret_cast<double*>(smb + L.ring);  // nr x m (stride m)
+  double* part = qs + (size_t)rp * m;                     // LG_NW x rp x (NH * 8)
+  double* Rr = part + (size_t)LG_NW * rp * NH * 8;        // nr x NVMAX
+  double* cr = Rr + (size_t)rp * NVMAX;                   // nr x NVMAX
   if (mode == 1 || mode == 2) {
     for (int idx = threadIdx.x; idx < nr * m; idx += LG_NT) {
       // consecutive threads: consecutive rows (agents) at one t -> the slot loads coalesce
       const int t = idx / nr, rl = idx - t * nr;
-      const int r = r_lo + rl;
-      const int ax = r / n, j = r - ax * n;
-      const int b = j >> 5, l = j & 31;
-      const double* qb = p.qbuf + (k & 1) * p.q_stride + ax * 32 + l;  // written by pass k
-      double v[2 * LG_MAXB];
-#pragma unroll
-      for (int e = 0; e < LG_MAXB; ++e) {
-        const int ent = blist[b * LG_MAXB + e];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const bool dg = (ent & 2) != 0;
-          const int u = (ent >> 2) + (dg ? t : 2 * t + h);
-          const bool ok = ent >= 0 && !(h == 1 && dg) && u >= cx.u_lo && u < cx.u_hi;
-          v[2 * e + h] = ok ? __ldcg(qb + (long long)u * 192 + (ent & 1) * 96) : 0.0;
-        }
-      }
       double qv = 0.0;
+      {
+        const int r = r_lo + rl;
+        const int ax = r / n, j = r - ax * n;
+        const int b = j >> 5, l = j & 31;
+        const double* qb = p.qbuf + (k & 1) * p.q_stride + ax * 32 + l;  // written by pass k
+        double v[2 * LG_MAXB];
 #pragma unroll
-      for (int e = 0; e < 2 * LG_MAXB; ++e) qv += v[e];
+        for (int e = 0; e < LG_MAXB; ++e) {
+          const int ent = blist[b * LG_MAXB + e];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const bool dg = (ent & 2) != 0;
+            const int u = (ent >> 2) + (dg ? t : 2 * t + h);
+            const bool ok = ent >= 0 && !(h == 1 && dg) && u >= cx.u_lo && u < cx.u_hi;
+            v[2 * e + h] = ok ? __ldcg(qb + (long long)u * 192 + (ent & 1) * 96) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 2 * LG_MAXB; ++e) qv += v[e];
+      }
       qs[rl * m + t] = qv;
     }
     __syncthreads();
     stamp(tsr, 8);
-  }
-  for (int rl = warp; rl < nr; rl += LG_NW) {
-    const int r = r_lo + rl;
-    const int ax = r / n, j = r - ax * n;
-    double c[NVMAX];
-    if (mode == 0) {
-      // straight-line coefficients (solver.py:327-330, packed on the host)
+    // 2. projection: warp w takes the k-steps w, w + LG_NW, ... of every row tile
+    {
+      const int g = lane >> 2, q = lane & 3;
+      const int ksn = (m + 3) >> 2;
+      for (int mt = 0; mt < mt_n; ++mt) {
+        double acc[NH][2];
 #pragma unroll
-      for (int q = 0; q < NVMAX; ++q) c[q] = q < p.nv ? p.c0[((long long)ax * n + j) * p.nv + q] : 0.0;
-    } else if (mode == 3) {
-      double mine = 0.0;
-      if (lane < NVMAX)
-        for (int g = 0; g < p.G; ++g) {
-          const double* src = p.xch[g] + (k & 1) * xstride + (long long)r * NVMAX + lane;
-          mine += p.sys_scope ? __ldcv(src) : __ldcg(src);
+        for (int h = 0; h < NH; ++h) acc[h][0] = acc[h][1] = 0.0;
+        for (int ks = warp; ks < ksn; ks += LG_NW) {
+          const int t = ks * 4 + q;
+          const double a = (t < m && mt * 8 + g < nr) ? qs[(mt * 8 + g) * m + t] : 0.0;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const int kk = h * 8 + g;
+            const double bv = (t < m && kk < NVMAX) ? Ps[t * NVMAX + kk] : 0.0;
+            dmma884(acc[h][0], acc[h][1], a, bv);
+          }
         }
+        double* pw = part + ((size_t)warp * rp + mt * 8 + g) * (NH * 8);
 #pragma unroll
-      for (int q = 0; q < NVMAX; ++q) c[q] = __shfl_sync(0xffffffffu, mine, q);
-    } else {
-#pragma unroll
-      for (int q = 0; q < NVMAX; ++q) c[q] = 0.0;
-      for (int t = lane; t < m; t += 32) {
-        const double qv = qs[rl * m + t];
-        const double* pr = Ps + t * NVMAX;
-#pragma unroll
-        for (int q = 0; q < NVMAX; ++q) c[q] = fma(qv, pr[q], c[q]);
+        for (int h = 0; h < NH; ++h) {
+          pw[h * 8 + 2 * q] = acc[h][0];
+          pw[h * 8 + 2 * q + 1] = acc[h][1];
+        }
       }
-      // butterfly: every lane ends with bitwise-identical sums (each stage adds the same two operands)
-#pragma unroll
-      for (int q = 0; q < NVMAX; ++q) c[q] = warp_sum(c[q]);
-      if (rl == warp) stamp(tsr, 9);
-      if (mode == 2) {
-        if (lane < NVMAX) {
-          double v = 0.0;
-#pragma unroll
-          for (int q = 0; q < NVMAX; ++q) v = (q == lane) ? c[q] : v;
-          p.xch[cx.g][(k & 1) * xstride + (long long)r * NVMAX + lane] = v;
-        }
-        continue;
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < nr * NVMAX; idx += LG_NT) {
+        const int rl = idx / NVMAX, kk = idx - rl * NVMAX;
+        double v = 0.0;
+        for (int w = 0; w < LG_NW; ++w) v += part[((size_t)w * rp + rl) * (NH * 8) + kk];
+        Rr[idx] = v;
       }
     }
-    lg_solve_row<NVMAX>(p, cx, mat, bbar, Ps, k, ax, j, c, mode != 0);
-    if (rl == warp) stamp(tsr, 10);
+    __syncthreads();
+    stamp(tsr, 9);
+    if (mode == 2) {
+      for (int idx = threadIdx.x; idx < nr * NVMAX; idx += LG_NT)
+        p.xch[cx.g][(k & 1) * xstride + (long long)r_lo * NVMAX + idx] = Rr[idx];
+    }
+  } else if (mode == 3) {
+    for (int idx = threadIdx.x; idx < nr * NVMAX; idx += LG_NT) {
+      double v = 0.0;
+      for (int g = 0; g < p.G; ++g) {
+        const double* src = p.xch[g] + (k & 1) * xstride + (long long)r_lo * NVMAX + idx;
+        v += p.sys_scope ? __ldcv(src) : __ldcg(src);
+      }
+      Rr[idx] = v;
+    }
+    __syncthreads();
   }
-  if (mode == 1 || mode == 2) {
-    // qs (generic-proxy writes/reads) lives in the ring the next P phase fills by TMA (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (mode != 2) {
+    // 3. coefficients (mode 0: the straight lines, solver.py:327-330, packed on the host)
+    const double rho = mat[SM::RHO];
+    for (int idx = threadIdx.x; idx < nr * NVMAX; idx += LG_NT) {
+      const int rl = idx / NVMAX, qo = idx - rl * NVMAX;
+      const int r = r_lo + rl;
+      const int ax = r / n, j = r - ax * n;
+      double cv;
+      if (mode == 0) {
+        cv = qo < p.nv ? p.c0[((long long)ax * n + j) * p.nv + qo] : 0.0;
+      } else {
+        const double* bj = p.beq + ((long long)ax * n + j) * 6;
+        double s1 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NVMAX; ++i) s1 = fma(mat[SM::G + qo * NVMAX + i], Rr[rl * NVMAX + i], s1);
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {
+          const double bm = bbar[ax * 6 + e];
+          s3 = fma(mat[SM::F + qo * 6 + e], __ldg(bj + e) - bm, s3);
+          s4 = fma(mat[SM::Fm + qo * 6 + e], bm, s4);
+        }
+        cv = rho * s1 + (s3 + s4);
+      }
+      cr[idx] = cv;
+      cx.cbuf[((long long)ax * n + j) * NVMAX + qo] = cv;
+    }
+    __syncthreads();
+    if (mode != 0) {
+      // boundary rows E c_j - beq_j (solver.py:448-452)
+      double bmx = 0.0;
+      for (int idx = threadIdx.x; idx < nr * 6; idx += LG_NT) {
+        const int rl = idx / 6, e = idx - rl * 6;
+        const int r = r_lo + rl;
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < NVMAX; ++i) v = fma(p.E[e * NVMAX + i], cr[rl * NVMAX + i], v);
+        bmx = fmax(bmx, fabs(v - __ldg(p.beq + (long long)r * 6 + e)));
+      }
+      bmx = warp_max(bmx);
+      if (lane == 0 && bmx > 0.0) atomicMax(cx.bnd + (k % 3), (unsigned long long)__double_as_longlong(bmx));
+    }
+    // 4. positions
+    for (int idx = threadIdx.x; idx < nr * m; idx += LG_NT) {
+      const int t = idx / nr, rl = idx - t * nr;
+      const int r = r_lo + rl;
+      const int ax = r / n, j = r - ax * n;
+      const double* pr = Ps + t * NVMAX;
+      const double* cj = cr + rl * NVMAX;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < NVMAX; ++q) v = fma(pr[q], cj[q], v);
+      cx.X[((long long)t * 3 + ax) * p.npad + j] = v;
+    }
+    stamp(tsr, 10);
   }
+  // the scratch (generic-proxy writes/reads) lives in the ring the next P phase fills by TMA
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   if (mode != 2 && threadIdx.x == 0 && nr > 0) {
     // publish: this CTA's rows of each agent block are in X (release after the CTA barrier)

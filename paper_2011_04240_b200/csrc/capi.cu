@@ -783,8 +783,13 @@ int run_large(st_plan* pl, bool f32, const double* c0, const double* beq, const 
   }
   const int cpg = grid / vgroups;
   if (cpg < 1) return fail(ST_EUNSUPPORTED, "too few SMs for the requested groups");
-  if ((long long)((3 * pl->n + cpg - 1) / cpg) * pl->m * 8 > sm.bar - sm.ring)
-    return fail(ST_EUNSUPPORTED, "large-fleet row reduction does not fit in shared memory");
+  {
+    // R-phase scratch in the multiplier ring: q rows | warp partials | R | c (am_large.cuh lg_rows)
+    const long long rp = ((3LL * pl->n + cpg - 1) / cpg + 7) / 8 * 8, nh8 = (pl->nvmax + 7) / 8 * 8;
+    const long long need = (rp * pl->m + (long long)swarm::LG_NW * rp * nh8 + 2 * rp * pl->nvmax) * 8;
+    if (need > sm.bar - sm.ring)
+      return fail(ST_EUNSUPPORTED, "large-fleet row reduction does not fit in shared memory");
+  }
   const LargeLayout Lg = large_layout(pl, G, cpg);
   const int n = pl->n, m = pl->m;
   // host tables: block pairs, group ranges, CTA ranges, multiplier offsets of this launch's units
