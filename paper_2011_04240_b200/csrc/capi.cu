@@ -478,7 +478,10 @@ bool large_eligible(const st_plan* pl, int batch, bool keep) {
   const char* e = std::getenv("SWARM_LARGE");
   const int mode = e ? std::atoi(e) : 1;
   if (mode == 0 || batch != 1 || keep || pl->nobs != 0 || pl->n < 2 || pl->n > 32 * swarm::LG_MAXB) return false;
-  return mode == 2 || pl->n > 64;
+  // n > 32: the whole-GPU unit decomposition beats the multi-cluster grid-barrier layout from the
+  // first multi-block size on (sph64j 3.12 -> 2.52 ms, rand48_s0 2.09 -> 1.80 ms; n <= 32 stays on
+  // one cluster: circ16j 0.98 vs 1.46 ms)
+  return mode == 2 || pl->n > 32;
 }
 
 // Units in block-pair-major order: a diagonal block pair (A == B) has one unit per sample t

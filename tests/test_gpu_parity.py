@@ -177,8 +177,11 @@ def test_results_independent_of_stale_device_memory(cuda_ok, name):
 def test_virtual_groups_reproduce_multi_cluster_bitwise(cuda_ok, name, groups, monkeypatch):
     """n <= 64 (multi-cluster kernel): the pair-sharded exchange (participants in per-group
     buffers, fixed participant order) run as `groups` virtual groups on one GPU must equal the
-    single-group multi-cluster solve bit for bit."""
+    single-group multi-cluster solve bit for bit.  (Single solves of 32 < n <= 64 run on the
+    large-fleet kernel by default; SWARM_LARGE=0 selects the multi-cluster layout, which keyed
+    and obstacle solves of that size still use.)"""
     from paper_2011_04240_b200 import FactorCache, SolverConfig, am_solve
+    monkeypatch.setenv("SWARM_LARGE", "0")
     spec, cfg, ref = load_golden(name)
     base = am_solve(spec, SolverConfig(max_iters=40), cache=FactorCache())
     monkeypatch.setenv("SWARM_VIRTUAL_GROUPS", str(groups))
@@ -189,7 +192,7 @@ def test_virtual_groups_reproduce_multi_cluster_bitwise(cuda_ok, name, groups, m
 
 
 @pytest.mark.parametrize("name,groups", [("rand256_s0", 2), ("rand256_s0", 3), ("rand256_s0", 8),
-                                         ("rand128_s0", 4)])
+                                         ("rand128_s0", 4), ("sph64j", 2), ("rand48_s0", 3)])
 def test_pair_sharded_groups_match_reference(cuda_ok, name, groups, monkeypatch):
     """n > 64 (large-fleet kernel): G pair-sharded groups -- each a contiguous range of agent
     pairs, its own partial right-hand sides exchanged once per iteration and summed in rank
