@@ -595,9 +595,11 @@ def _am_solve_batch(specs, config, cache, with_metrics) -> list:
     spec0 = specs[0]
     n, n_obs = len(spec0.start), len(spec0.obstacles)
     basis = poly.for_spec(spec0)
-    report_path = not config.keep_state and basis.num_samples >= 3 and native.load().swarm_has_report
+    # the device report pass: one warp's (m x 3) positions in shared memory (m <= 2000 here), one
+    # launch covers at most 65535 scenarios (grid y of the collision rows)
+    report_path = (not config.keep_state and 3 <= basis.num_samples <= 2000 and native.load().swarm_has_report)
     B = len(specs)
-    K = _pipeline_chunks(B) if report_path else 1
+    K = max(_pipeline_chunks(B), -(-B // 65535)) if report_path else 1
     bounds = [B * i // K for i in range(K + 1)]
     prep = _prep_chunk(specs[: bounds[1]], basis, n_obs)
     fp = kkt.fingerprint(basis, n, n_obs)
