@@ -87,3 +87,21 @@ def test_pipeline_chunking_rule(monkeypatch):
     assert engine._pipeline_chunks(1024) == 3
     monkeypatch.setenv("SWARM_PIPE_CHUNKS", "5")
     assert engine._pipeline_chunks(3) == 3 and engine._pipeline_chunks(100) == 5
+
+
+@pytest.mark.gpu
+def test_pooled_trajectory_buffers_are_never_shared_with_live_reports(cuda_ok):
+    """Report trajectories live in pooled page-locked buffers: a buffer goes back to the pool only
+    when every array over it is gone, so later calls never overwrite reports still held."""
+    import gc
+
+    from paper_2011_04240_b200 import am_solve_batch
+    a = am_solve_batch(_specs(8))
+    keep = [r.trajectories.copy() for r in a]
+    for seed in (100, 200, 300):
+        am_solve_batch(_specs(8, seed0=seed))  # dropped at once: their buffer returns to the pool
+        gc.collect()
+    b = am_solve_batch(_specs(8, seed0=400))
+    for r, t in zip(a, keep):
+        assert np.array_equal(r.trajectories, t)
+    assert not any(np.shares_memory(x.trajectories, y.trajectories) for x in a for y in b)
