@@ -39,14 +39,18 @@ using KernelFn = void (*)(swarm::KParams);
 struct KernelEntry {
   int NB, NT, NVMAX, LAM;
   bool f32;  // FP32 pair state (multipliers and pair arithmetic in FP32, FP64 solve)
+  bool obs_free;  // obstacle rows compiled out (scenarios without obstacles only)
   KernelFn fn;
 };
 
 using swarm::am_cluster_kernel;
 constexpr int kS = swarm::LAM_SMEM, kG = swarm::LAM_GLOBAL, kK = swarm::LAM_GLOBAL_KEEP;
-#define ST_K(NB, NT, NV, L, F) {NB, NT, NV, L, F, am_cluster_kernel<NB, NT, NV, L, F>}
+#define ST_K(NB, NT, NV, L, F) {NB, NT, NV, L, F, false, am_cluster_kernel<NB, NT, NV, L, F>}
+#define ST_K0(NB, NT, NV, L, F) {NB, NT, NV, L, F, true, am_cluster_kernel<NB, NT, NV, L, F, false>}
 // lambda fits in shared memory only for n <= 32 (NB == 1); larger fleets stream it from L2.
 const KernelEntry kKernels[] = {
+    // obstacle-free variants first (the batch bench and the common single solves)
+    ST_K0(1, 512, 12, kS, false), ST_K0(1, 512, 12, kG, false),
     ST_K(1, 512, 12, kS, false), ST_K(1, 512, 12, kG, false), ST_K(1, 512, 12, kK, false),
     ST_K(1, 512, 16, kS, false), ST_K(1, 512, 16, kG, false), ST_K(1, 512, 16, kK, false),
     ST_K(2, 384, 12, kG, false), ST_K(2, 384, 12, kK, false), ST_K(2, 384, 16, kG, false),
@@ -59,6 +63,7 @@ const KernelEntry kKernels[] = {
     ST_K(8, 256, 12, kG, true),  ST_K(8, 256, 12, kK, true),
 };
 #undef ST_K
+#undef ST_K0
 
 struct Launch {
   int NVMAX = 0;
@@ -228,9 +233,9 @@ int tail_rows(const Launch& L, long long spare) {
   return (int)std::max(0LL, std::min(rows_max, spare / per_row));
 }
 
-const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, bool f32) {
+const KernelEntry* find_kernel(int NB, int NVMAX, int LAM, bool f32, bool obstacles) {
   for (const auto& e : kKernels)
-    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM && e.f32 == f32) return &e;
+    if (e.NB == NB && e.NVMAX == NVMAX && e.LAM == LAM && e.f32 == f32 && (!obstacles || !e.obs_free)) return &e;
   return nullptr;
 }
 
@@ -242,7 +247,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
   const int nb_need = n <= 32 ? 1 : ceil_div(n, 32);
   int NB = 0;
   for (int cand : {1, 2, 4, 8})
-    if (cand >= nb_need && find_kernel(cand, pl->nvmax, swarm::LAM_GLOBAL, f32)) { NB = cand; break; }
+    if (cand >= nb_need && find_kernel(cand, pl->nvmax, swarm::LAM_GLOBAL, f32, pl->nobs > 0)) { NB = cand; break; }
   if (!NB) return fail(ST_EUNSUPPORTED, "no compiled kernel for this agent count and basis degree");
   L.NB = NB;
   L.NVMAX = pl->nvmax;
@@ -303,7 +308,7 @@ int choose_launch(st_plan* pl, int batch, int hint, bool keep, Launch& L, int G 
     if (cg_try == 1 && pass == 0) continue;  // coefficients in global memory only with lambda there too
     const int lam = pass == 0 ? swarm::LAM_SMEM : (keep ? swarm::LAM_GLOBAL_KEEP : swarm::LAM_GLOBAL);
     if (keep && pass == 0) continue;
-    const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam, f32);
+    const KernelEntry* ke = find_kernel(NB, pl->nvmax, lam, f32, pl->nobs > 0);
     if (!ke) continue;
     const long long bud = budget;
     if ((long long)C * G > pl->m || C < 1 || C > 16) continue;  // every CTA owns >= 1 sample

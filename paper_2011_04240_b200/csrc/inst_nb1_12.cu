@@ -6,4 +6,6 @@ namespace swarm {
 template __global__ void am_cluster_kernel<1, 512, 12, 0, false>(const KParams);
 template __global__ void am_cluster_kernel<1, 512, 12, 1, false>(const KParams);
 template __global__ void am_cluster_kernel<1, 512, 12, 2, false>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 12, 0, false, false>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 12, 1, false, false>(const KParams);
 }  // namespace swarm
