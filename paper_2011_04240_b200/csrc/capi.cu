@@ -56,6 +56,7 @@ const KernelEntry kKernels[] = {
     ST_K(2, 384, 12, kG, false), ST_K(2, 384, 12, kK, false), ST_K(2, 384, 16, kG, false),
     ST_K(2, 384, 16, kK, false), ST_K(4, 256, 12, kG, false), ST_K(4, 256, 12, kK, false),
     ST_K(8, 256, 12, kG, false), ST_K(8, 256, 12, kK, false),
+    ST_K0(1, 512, 12, kS, true), ST_K0(1, 512, 12, kG, true),
     ST_K(1, 512, 12, kS, true),  ST_K(1, 512, 12, kG, true),  ST_K(1, 512, 12, kK, true),
     ST_K(1, 512, 16, kS, true),  ST_K(1, 512, 16, kG, true),  ST_K(1, 512, 16, kK, true),
     ST_K(2, 384, 12, kG, true),  ST_K(2, 384, 12, kK, true),  ST_K(2, 384, 16, kG, true),

@@ -9,4 +9,6 @@ template __global__ void am_cluster_kernel<1, 512, 12, 2, true>(const KParams);
 template __global__ void am_cluster_kernel<1, 512, 16, 0, true>(const KParams);
 template __global__ void am_cluster_kernel<1, 512, 16, 1, true>(const KParams);
 template __global__ void am_cluster_kernel<1, 512, 16, 2, true>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 12, 0, true, false>(const KParams);
+template __global__ void am_cluster_kernel<1, 512, 12, 1, true, false>(const KParams);
 }  // namespace swarm
