@@ -649,8 +649,8 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   // opt-in phase timers: SWARM_PHASE_TIMERS=1 prints per-phase cycles of scenario 0, CTA 0
   static long long* d_ts = nullptr;
   const bool timers = std::getenv("SWARM_PHASE_TIMERS") != nullptr;
-  if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 256 * 16 * sizeof(long long)));
-  if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 256 * 16 * sizeof(long long), s));
+  if (timers && !d_ts) ST_CUDA(cudaMalloc(&d_ts, 16 * 4096 * sizeof(long long)));
+  if (timers) ST_CUDA(cudaMemsetAsync(d_ts, 0, 16 * 4096 * sizeof(long long), s));
   k.tstamp = timers ? d_ts : nullptr;
   ST_CUDA(cudaMemsetAsync(pl->d_counter, 0, sizeof(int), s));
   cudaLaunchConfig_t cfg = {};
@@ -733,7 +733,7 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
   // whatever streams their callers use (advice r1: st_solve_device on several streams)
   ST_CUDA(cudaEventRecord(pl->ev_done, s));
   if (timers) {
-    std::vector<long long> h(256 * 16);
+    std::vector<long long> h(16 * 4096);
     ST_CUDA(cudaMemcpyAsync(h.data(), d_ts, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
     static const char* names[] = {"pull+test", "solve", "bar2", "gather", "positions", "pairwise", "warp-wait",
@@ -758,6 +758,30 @@ int run(st_plan* pl, const Launch& L0, int batch, const double* c0, const double
       }
       std::fprintf(stderr, " [project: drain=%.0f combine=%.0f sync=%.0f basis=%.0f]\n", drain / cnt, sub[0] / cnt,
                    sub[1] / cnt, sub[2] / cnt);
+      // SWARM_PHASE_TIMERS=2: the same per-phase averages for every CTA of the first cluster
+      // (each on its own SM clock): who arrives last at the cluster barriers
+      if (std::atoi(std::getenv("SWARM_PHASE_TIMERS")) == 2) {
+        for (int r = 0; r < std::min(L.C, 16); ++r) {
+          double a2[9] = {0};
+          for (int it = 1; it <= cnt; ++it) {
+            const long long* t = &h[r * 4096 + 16 * it];
+            for (int q = 0; q < 8; ++q) a2[q] += t[q + 1] - t[q];
+            a2[8] += h[r * 4096 + 16 * (it + 1)] - t[8];
+          }
+          double b2[4] = {0};
+          for (int it = 1; it <= cnt; ++it) {
+            const long long* t = &h[r * 4096 + 16 * it];
+            b2[0] += t[12] - t[0];   // pull: norms
+            b2[1] += t[13] - t[12];  // pull: owner rows
+            b2[2] += t[15] - t[1];   // test (owner mode)
+            b2[3] += t[14] - t[15];  // solve compute
+          }
+          std::fprintf(stderr, "   cta %2d:", r);
+          for (int q = 0; q < 9; ++q) std::fprintf(stderr, " %s=%.0f", names[q], a2[q] / cnt);
+          std::fprintf(stderr, " | norms=%.0f rows=%.0f test=%.0f solvec=%.0f\n", b2[0] / cnt, b2[1] / cnt,
+                       b2[2] / cnt, b2[3] / cnt);
+        }
+      }
     }
   }
   return 0;

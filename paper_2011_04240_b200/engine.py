@@ -259,12 +259,14 @@ def boundary_arrays(specs) -> np.ndarray:
     One C-level pass over the state objects (attribute getters feeding ``np.fromiter``):
     the batch entry touches no per-agent Python beyond it."""
     B, n = len(specs), len(specs[0].start)
-    get = attrgetter("position", "velocity", "acceleration")
     chain = itertools.chain.from_iterable
-    states = [st for spec in specs for side in (spec.start, spec.goal) for st in side]
-    flat = np.fromiter(chain(chain(map(get, states))), dtype=float, count=len(states) * 9)
-    # flat order: scenario, start/goal, agent, pos/vel/acc, axis
-    return flat.reshape(B, 2, n, 3, 3).transpose(0, 1, 3, 2, 4)
+    states = list(chain(side for spec in specs for side in (spec.start, spec.goal)))
+    out = np.empty((3, len(states), 3))
+    for f, name in enumerate(("position", "velocity", "acceleration")):
+        out[f] = np.fromiter(chain(map(attrgetter(name), states)), dtype=float,
+                             count=len(states) * 3).reshape(-1, 3)
+    # out order: pos/vel/acc, (scenario, start/goal, agent), axis
+    return out.reshape(3, B, 2, n, 3).transpose(1, 2, 0, 3, 4)
 
 
 def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None):
@@ -455,7 +457,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
     metrics_s = (time.perf_counter() - tc0) / B
     iters = out["iters"].tolist()
     conv = out["converged"].tolist()
-    hist = out["hist"].tolist()  # one conversion for the whole batch; histories are list slices
+    hist = out["hist"]
     common = {"assembly_s": t1 - t0, "factorization_s": t2 - t1, "loop_s": loop_ms / 1e3, "h2d_s": h2d_ms / 1e3,
               "d2h_s": d2h_ms / 1e3, "solve_call_s": t3 - t2, "metrics_s": metrics_s, "batch": B}
     loop_s = loop_ms / 1e3
@@ -478,8 +480,7 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
                 "mean_arc_length": arc_mean[b],
                 "mean_smoothness": smooth_mean[b],
             }
-        h0, h1, h2 = hist[b]
-        h0, h1, h2 = h0[:it], h1[:it], h2[:it]
+        h0, h1, h2 = hist[b, :, :it].tolist()  # only the iterations run become Python floats
         timings = dict(common)
         timings["per_iteration_s"] = loop_s / max(1, it)
         timings["total_s"] = time.perf_counter() - t0

@@ -123,7 +123,9 @@ def straight_line(basis: Basis, start: np.ndarray, goal: np.ndarray) -> np.ndarr
     nv = basis.num_coeffs
     if basis.kind == BasisKind.BERNSTEIN:
         frac = np.arange(nv) / basis.degree
-        return start[..., None] + frac * (goal - start)[..., None]
+        out = np.multiply.outer(np.subtract(goal, start, order="C"), frac)  # = s + frac (g - s), bitwise
+        out += start[..., None]
+        return out
     out = np.zeros(start.shape + (nv,))
     out[..., 0] = start
     out[..., 1] = goal - start

@@ -207,18 +207,29 @@ def validate_batch(specs, start_pos: np.ndarray, goal_pos: np.ndarray) -> list:
     n = start_pos.shape[1]
     geo = np.array([(s.geometry.l_xy, s.geometry.l_z) for s in specs], dtype=float)
     scale = np.stack([1.0 / geo[:, 0], 1.0 / geo[:, 0], 1.0 / geo[:, 1]], axis=1)[:, None, :]
-    ii, jj = _pairs(n) if n > 1 else (np.zeros(0, int), np.zeros(0, int))
+    upper = np.triu(np.ones((n, n), dtype=bool), 1)
     cand = {}
     for label, P in (("start", start_pos), ("goal", goal_pos)):
-        if n > 1:
-            # |pi - pj|^2 = |pi|^2 + |pj|^2 - 2 pi.pj on the scaled positions (one batched matmul);
-            # a loose prefilter -- every candidate is re-checked with the exact scalar expression
-            Ps = np.ascontiguousarray(P) * scale
+        if n < 2:
+            continue
+        # |pi - pj|^2 = |pi|^2 + |pj|^2 - 2 pi.pj on the scaled positions (batched matmul, in place,
+        # over cache-sized slices of the batch); a loose prefilter -- every candidate is re-checked
+        # with the exact scalar expression.  np.nonzero walks (b, i, j) in the pair order i < j.
+        step = max(1, (1 << 18) // (n * n))
+        for b0 in range(0, B, step):
+            Ps = P[b0: b0 + step] * scale[b0: b0 + step]
             sq = np.einsum("bnk,bnk->bn", Ps, Ps)
-            d2 = sq[:, :, None] + sq[:, None, :] - 2.0 * np.matmul(Ps, Ps.transpose(0, 2, 1))
-            near = d2[:, ii, jj] < 1.0 + 1e-6 * (1.0 + sq[:, ii] + sq[:, jj])
-            for b, pk in zip(*np.nonzero(near)):
-                cand.setdefault(int(b), []).append((label, 0, int(ii[pk]), int(jj[pk])))
+            d2 = np.matmul(Ps, Ps.transpose(0, 2, 1))
+            d2 *= -2.0
+            tol = sq * (1.0 - 1e-6)  # d2 < 1 + 1e-6 (1 + sq_i + sq_j)
+            d2 += tol[:, :, None]
+            d2 += tol[:, None, :]
+            near = d2 < 1.0 + 1e-6
+            near &= upper
+            if not near.any():
+                continue
+            for b, i, j in zip(*np.nonzero(near)):
+                cand.setdefault(int(b) + b0, []).append((label, 0, int(i), int(j)))
     obs_any = any(s.obstacles for s in specs)
     for b in range(B):
         if b not in cand and not obs_any:

@@ -3,7 +3,7 @@ and the C8 obstacle family; the latency breakdown of small single solves."""
 import os
 import sys
 
-os.environ["SWARM_PHASE_TIMERS"] = "1"
+os.environ.setdefault("SWARM_PHASE_TIMERS", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2011_04240_b200 import SolverConfig, am_solve, generate_random_with_obstacles, named  # noqa: E402
 
