@@ -1207,8 +1207,12 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   // small solves (single scenarios): inputs and the small outputs go through one page-locked
   // staging buffer -- one H2D and one D2H instead of a pageable copy per array
   const size_t small_out = (n_c + n_h) * 8 + 2 * (size_t)batch * 4 + (rep ? (size_t)batch * (2 * n + 2) * 8 : 0);
-  const bool staged = !keep && in_bytes + small_out <= ((size_t)1 << 20);
-  if (staged && in_bytes + small_out > pl->stage_bytes) {
+  // the report pass's collision inputs (per-scenario geometry and obstacle rows) ride in the same
+  // staging buffer, right after the solve inputs (a pageable copy would block the host)
+  const bool rep_verdict = rep && (rep->min_dist || rep->n_viol);
+  const size_t rep_in = rep_verdict ? (size_t)batch * 16 + (size_t)batch * pl->nobs * 40 : 0;
+  const bool staged = !keep && in_bytes + rep_in + small_out <= ((size_t)1 << 20);
+  if (staged && in_bytes + rep_in + small_out > pl->stage_bytes) {
     if (pl->h_stage) cudaFreeHost(pl->h_stage);
     pl->h_stage = nullptr;
     pl->stage_bytes = 0;
@@ -1221,6 +1225,10 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     memcpy(hs, c0, n_c * 8);
     memcpy(hs + n_c, beq, n_b * 8);
     memcpy(hs + n_c + n_b, geom, n_g * 8);
+    if (rep_verdict) {
+      memcpy((char*)hs + in_bytes, rep->geom2, (size_t)batch * 16);
+      if (pl->nobs) memcpy((char*)hs + in_bytes + (size_t)batch * 16, rep->obs, (size_t)batch * pl->nobs * 40);
+    }
     ST_CUDA(cudaMemcpyAsync(d_c0, hs, in_bytes, cudaMemcpyHostToDevice, s));
   } else {
     ST_CUDA(cudaMemcpyAsync(d_c0, c0, n_c * 8, cudaMemcpyHostToDevice, s));
@@ -1265,8 +1273,11 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     rep_small = r_arc;
     const bool verdict = rep->min_dist || rep->n_viol;
     if (verdict) {
-      ST_CUDA(cudaMemcpyAsync(r_geom, rep->geom2, (size_t)batch * 16, cudaMemcpyHostToDevice, s));
-      if (n_obs) ST_CUDA(cudaMemcpyAsync(r_obs, rep->obs, (size_t)batch * n_obs * 40, cudaMemcpyHostToDevice, s));
+      const char* g2 = staged ? (const char*)hs + in_bytes : (const char*)rep->geom2;  // page-locked when staged
+      ST_CUDA(cudaMemcpyAsync(r_geom, g2, (size_t)batch * 16, cudaMemcpyHostToDevice, s));
+      if (n_obs)
+        ST_CUDA(cudaMemcpyAsync(r_obs, staged ? g2 + (size_t)batch * 16 : (const char*)rep->obs,
+                                (size_t)batch * n_obs * 40, cudaMemcpyHostToDevice, s));
     }
     ST_CUDA(swarm_report_launch(batch, n, m, nv, pl->nvmax, d_cout, pl->P, r_traj, r_arc, r_smooth, s));
     if (verdict) {

@@ -31,7 +31,7 @@ from operator import attrgetter
 import numpy as np
 
 from . import kkt, metrics, native, poly
-from .spec import obstacle_axes, validate, validate_batch
+from .spec import obstacle_axes, validate, validate_batch, validate_positions
 
 log = logging.getLogger(__name__)
 
@@ -269,7 +269,7 @@ def boundary_arrays(specs) -> np.ndarray:
     return out.reshape(3, B, 2, n, 3).transpose(1, 2, 0, 3, 4)
 
 
-def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None):
+def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None, obs_rows: np.ndarray | None = None):
     """Scenario batch -> (c0 (B,3,n,nv), b_eq (B,3,n,6), geom (B, 2+5 n_obs)).
 
     b_eq rows per agent and axis: [pos0, vel0, acc0, posT, velT, accT]
@@ -286,10 +286,10 @@ def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None):
     geom = np.empty((B, 2 + 5 * n_obs))
     geom[:, :2] = [(spec.geometry.l_xy, spec.geometry.l_z) for spec in specs]
     if n_obs:
-        for b, spec in enumerate(specs):
-            for k, obs in enumerate(spec.obstacles):
-                lxy, lz = obstacle_axes(spec, obs)
-                geom[b, 2 + 5 * k: 7 + 5 * k] = (*obs.center, lxy, lz)
+        if obs_rows is None:  # (B, n_obs, 5): centre, l_xy/2 + R, l_z/2 + R (problem.py:136-141)
+            obs_rows = np.array([[[*o.center, *obstacle_axes(spec, o)] for o in spec.obstacles] for spec in specs],
+                                dtype=float)
+        geom[:, 2:] = obs_rows.reshape(B, 5 * n_obs)
     return c0, beq, geom
 
 
@@ -453,7 +453,9 @@ def _make_reports(specs, out, basis, plan, cache, schedule, config, stamps, with
             mins, counts = [x[0] for x in cols], [x[1] for x in cols]
             arc, smooth = metrics.trajectory_metrics_batch_coeffs(c, basis.P)
         arc_l, smooth_l = arc.tolist(), smooth.tolist()
-        arc_mean, smooth_mean = arc.mean(axis=1).tolist(), smooth.mean(axis=1).tolist()
+        # == arc.mean(axis=1) bit for bit (the same add.reduce, then one true division)
+        arc_mean = (np.add.reduce(arc, axis=1) / arc.shape[1]).tolist()
+        smooth_mean = (np.add.reduce(smooth, axis=1) / smooth.shape[1]).tolist()
     metrics_s = (time.perf_counter() - tc0) / B
     iters = out["iters"].tolist()
     conv = out["converged"].tolist()
@@ -560,23 +562,27 @@ def _prep_chunk(specs, basis, n_obs):
     """Validation (raises before this chunk's device work) and packing of one chunk."""
     t0 = time.perf_counter()
     bnd = boundary_arrays(specs)
+    # obstacle rows (centre, l_xy/2 + R, l_z/2 + R): validation prefilter, kernel geometry, collision rows
+    col_obs = (np.stack([metrics._obstacle_rows(sp.geometry, sp.obstacles) for sp in specs]) if n_obs
+               else np.zeros((len(specs), 0, 5)))
     if len(specs) == 1:  # the per-spec check: no batch-vectorization overhead for single solves
-        v = validate(specs[0])
+        v = validate_positions(specs[0], bnd[0, 0, 0], bnd[0, 1, 0], col_obs[0])
         if v:
             raise _infeasible(v)
     else:
-        for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0]):
+        for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0], col_obs):
             if v:
                 raise _infeasible(v)
-    c0, beq, geom = pack(specs, basis, bnd)
-    col_geom = np.array([[sp.geometry.l_xy, sp.geometry.l_z] for sp in specs], dtype=float).reshape(-1, 2)
-    col_obs = (np.stack([metrics._obstacle_rows(sp.geometry, sp.obstacles) for sp in specs]) if n_obs
-               else np.zeros((len(specs), 0, 5)))
+    c0, beq, geom = pack(specs, basis, bnd, col_obs)
+    col_geom = geom[:, :2]
     return t0, time.perf_counter(), c0, beq, geom, col_geom, col_obs
 
 
 def _check_finite(out, offset: int = 0) -> None:
-    bad = np.flatnonzero(out["status"] == native.ST_NONFINITE)
+    flags = out["status"] == native.ST_NONFINITE
+    if not flags.any():
+        return
+    bad = np.flatnonzero(flags)
     if bad.size:
         raise NonFiniteStateError(
             f"non-finite pair state (d/beta out of range) in iteration {int(out['iters'][bad[0]])} of scenario "

@@ -31,6 +31,7 @@ fingerprint, none inside the loop; kkt_cache.py:385-419).
 
 from __future__ import annotations
 
+import functools
 import hashlib
 import json
 import logging
@@ -69,6 +70,7 @@ class RhoSchedule:
         return self.values[self.stage_for(iteration)]
 
 
+@functools.lru_cache(maxsize=64)
 def build_rho_schedule(rho_initial: float, growth: float, stages: int, max_iters: int) -> RhoSchedule:
     if not rho_initial > 0:
         raise ValueError(f"rho_initial must be positive, got {rho_initial}")

@@ -194,11 +194,65 @@ def validate(spec) -> list[Violation]:
     return out
 
 
-def validate_batch(specs, start_pos: np.ndarray, goal_pos: np.ndarray) -> list:
+def _obstacle_candidates(P, obs_rows):
+    """(..., n, 3) positions x (..., k, 5) obstacle rows (centre, l_xy/2 + R, l_z/2 + R) -> (..., n, k)
+    mask of the (agent, obstacle) pairs whose normalized separation may be < 1 (loose prefilter)."""
+    d = P[..., :, None, :] - obs_rows[..., None, :, :3]
+    d[..., :2] /= obs_rows[..., None, :, 3:4]
+    d[..., 2] /= obs_rows[..., None, :, 4]
+    return np.einsum("...c,...c->...", d, d) < (1.0 + 1e-9) ** 2
+
+
+def validate_positions(spec, start_pos: np.ndarray, goal_pos: np.ndarray, obs_rows=None) -> list[Violation]:
+    """``validate`` of one spec from its (n, 3) start / goal position arrays (``engine.boundary_arrays``)
+    and, with obstacles, its (k, 5) obstacle rows: the same violations, order and text; one vectorized
+    prefilter over both endpoints, the reference's scalar expression on each candidate."""
+    out: list[Violation] = []
+    g = spec.geometry
+    n = start_pos.shape[0]
+    P2 = np.stack([start_pos, goal_pos])
+    near = None
+    if n > 1:
+        ii, jj = _pairs(n)
+        d = (P2[:, ii] - P2[:, jj]) * np.array([1.0 / g.l_xy, 1.0 / g.l_xy, 1.0 / g.l_z])
+        near = np.einsum("spk,spk->sp", d, d) < (1.0 + 1e-9) ** 2
+        if not near.any():
+            near = None
+    near_o = None
+    if spec.obstacles:
+        if obs_rows is None:
+            obs_rows = np.array([[*o.center, *obstacle_axes(spec, o)] for o in spec.obstacles], dtype=float)
+        near_o = _obstacle_candidates(P2, obs_rows)
+        if not near_o.any():
+            near_o = None
+    if near is None and near_o is None:
+        return out
+    for side, label in enumerate(("start", "goal")):
+        P = P2[side]
+        if near is not None:
+            for p in np.flatnonzero(near[side]).tolist():
+                i, j = int(ii[p]), int(jj[p])
+                sep = _separation(P[i].tolist(), P[j].tolist(), g.l_xy, g.l_z)
+                if sep < 1.0:
+                    out.append(Violation(f"{label} pair ({i}, {j})", f"normalized separation {sep:.4f} < 1"))
+        if near_o is not None:
+            for i, k in zip(*np.nonzero(near_o[side])):
+                obs = spec.obstacles[k]
+                lxy, lz = obstacle_axes(spec, obs)
+                sep = _separation(P[i].tolist(), obs.center, lxy, lz)
+                if sep < 1.0:
+                    out.append(Violation(f"{label} agent {int(i)} vs obstacle {int(k)}",
+                                         f"normalized separation {sep:.4f} < 1"))
+    return out
+
+
+def validate_batch(specs, start_pos: np.ndarray, goal_pos: np.ndarray, obs_rows=None) -> list:
     """``validate`` of B same-shape specs at once: the same violations, order and text per spec.
 
-    start_pos / goal_pos: (B, n, 3) positions (``engine.boundary_arrays``).  One vectorized
-    prefilter over every pair of every spec; only candidate pairs run the scalar expression.
+    start_pos / goal_pos: (B, n, 3) positions (``engine.boundary_arrays``); obs_rows: (B, k, 5)
+    obstacle rows (centre, l_xy/2 + R, l_z/2 + R), built here when omitted.  One vectorized
+    prefilter over every pair and every (agent, obstacle) row of every spec; only candidates run
+    the scalar expression.
     """
     B = len(specs)
     out = [[] for _ in range(B)]
@@ -230,27 +284,38 @@ def validate_batch(specs, start_pos: np.ndarray, goal_pos: np.ndarray) -> list:
                 continue
             for b, i, j in zip(*np.nonzero(near)):
                 cand.setdefault(int(b) + b0, []).append((label, 0, int(i), int(j)))
-    obs_any = any(s.obstacles for s in specs)
-    for b in range(B):
-        if b not in cand and not obs_any:
-            continue
+    k_obs = len(specs[0].obstacles)
+    if k_obs:
+        if obs_rows is None:
+            obs_rows = np.array([[[*o.center, *obstacle_axes(s, o)] for o in s.obstacles] for s in specs],
+                                dtype=float)
+        step = max(1, (1 << 18) // (n * k_obs))
+        for label, P in (("start", start_pos), ("goal", goal_pos)):
+            for b0 in range(0, B, step):
+                near_o = _obstacle_candidates(P[b0: b0 + step], obs_rows[b0: b0 + step])
+                if not near_o.any():
+                    continue
+                for b, i, k in zip(*np.nonzero(near_o)):  # (b, i, k) in the reference's loop order
+                    cand.setdefault(int(b) + b0, []).append((label, 1, int(i), int(k)))
+    for b, entries in cand.items():
         spec = specs[b]
         g = spec.geometry
-        entries = cand.get(b, [])
         for label, P in (("start", start_pos), ("goal", goal_pos)):
-            for lab, _, i, j in entries:
-                if lab != label:
+            for lab, kind, i, j in entries:  # per label: pairs first, then (agent, obstacle) rows
+                if lab != label or kind != 0:
                     continue
                 sep = _separation(P[b, i], P[b, j], g.l_xy, g.l_z)
                 if sep < 1.0:
                     out[b].append(Violation(f"{label} pair ({i}, {j})", f"normalized separation {sep:.4f} < 1"))
-            for i in range(n):
-                for k, obs in enumerate(spec.obstacles):
-                    lxy, lz = obstacle_axes(spec, obs)
-                    sep = _separation(P[b, i], obs.center, lxy, lz)
-                    if sep < 1.0:
-                        out[b].append(Violation(f"{label} agent {i} vs obstacle {k}",
-                                                f"normalized separation {sep:.4f} < 1"))
+            for lab, kind, i, k in entries:
+                if lab != label or kind != 1:
+                    continue
+                obs = spec.obstacles[k]
+                lxy, lz = obstacle_axes(spec, obs)
+                sep = _separation(P[b, i], obs.center, lxy, lz)
+                if sep < 1.0:
+                    out[b].append(Violation(f"{label} agent {i} vs obstacle {k}",
+                                            f"normalized separation {sep:.4f} < 1"))
     return out
 
 

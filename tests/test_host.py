@@ -283,6 +283,46 @@ def test_vectorized_validate_equals_scalar_loop():
     assert total > 0
 
 
+def test_position_and_batch_validation_equal_validate():
+    """The array-fed validators of the solve path (single: validate_positions, batch: validate_batch,
+    both with the obstacle prefilter) report validate's violations, order and text, obstacles included."""
+    import dataclasses
+
+    from paper_2011_04240_b200 import metrics
+    from paper_2011_04240_b200.spec import Obstacle as Ob, validate, validate_batch, validate_positions
+
+    rng = np.random.default_rng(5)
+    specs, total = [], 0
+    for trial in range(30):
+        n = int(rng.integers(1, 20))
+        spec = generate_random(n, (8, 8, 3), 0.4, trial)
+        scale = rng.uniform(0.05, 1)
+        starts = tuple(dataclasses.replace(s, position=tuple((np.array(s.position) * scale).tolist()))
+                       for s in spec.start)
+        obs = tuple(Ob(center=tuple(rng.uniform(-4, 4, 3).tolist()), radius=float(rng.uniform(0.2, 1.5)))
+                    for _ in range(3))
+        specs.append(dataclasses.replace(spec, start=starts, obstacles=obs))
+    for spec in specs:
+        bnd = engine.boundary_arrays([spec])
+        rows = metrics._obstacle_rows(spec.geometry, spec.obstacles)
+        want = validate(spec)
+        assert validate_positions(spec, bnd[0, 0, 0], bnd[0, 1, 0], rows) == want
+        assert validate_positions(spec, bnd[0, 0, 0], bnd[0, 1, 0]) == want
+        total += sum("obstacle" in v.subject for v in want)
+    assert total > 0
+    for n in (1, 3, 11):  # a batch shares one shape: rebuild the specs at n agents
+        group = []
+        for trial, base in enumerate(specs[:8]):
+            spec = generate_random(n, (8, 8, 3), 0.4, 100 + trial)
+            starts = tuple(dataclasses.replace(s, position=tuple((np.array(s.position) * 0.2).tolist()))
+                           for s in spec.start)
+            group.append(dataclasses.replace(spec, start=starts, obstacles=base.obstacles))
+        bnd = engine.boundary_arrays(group)
+        rows = np.stack([metrics._obstacle_rows(g.geometry, g.obstacles) for g in group])
+        assert validate_batch(group, bnd[:, 0, 0], bnd[:, 1, 0], rows) == [validate(g) for g in group]
+        assert validate_batch(group, bnd[:, 0, 0], bnd[:, 1, 0]) == [validate(g) for g in group]
+
+
 def test_vectorized_trajectory_metrics_bitwise():
     from paper_2011_04240_b200 import metrics
     rng = np.random.default_rng(3)
