@@ -446,8 +446,9 @@ def main():
     if world == 1:
         from paper_2011_04240_b200 import am_solve_batch
         am_solve_batch(specs, cfg, cache=cache)
-        best = None
+        best, reps = None, None
         for _ in range(3):
+            reps = None  # the previous call's reports are freed outside the timed region
             t0 = time.perf_counter()
             reps = am_solve_batch(specs, cfg, cache=cache)
             dt = time.perf_counter() - t0

@@ -102,8 +102,20 @@ int st_solve_report(st_plan* plan, int batch, const double* c0, const double* b_
                     const double* col_obs, double* traj, double* arc, double* smooth, double* min_dist,
                     long long* n_viol);
 
+/* st_solve_report in two halves, for pipelining host work against the device: _begin copies
+ * the inputs and enqueues the solve, the report pass and every output copy, and returns;
+ * st_solve_end waits for them and returns the timings.  Output arrays must be page-locked
+ * (st_host_alloc) or _begin blocks until the device is done.  One begun solve per plan:
+ * every other host-pointer call on the plan fails (ST_EINVAL) until st_solve_end. */
+int st_solve_report_begin(st_plan* plan, int batch, const double* c0, const double* b_eq, const double* geom,
+                          int switch_every, int max_iters, double tol, int flags, int cluster_hint,
+                          double* c_out, double* hist, int* iters, int* converged, const double* col_geom,
+                          const double* col_obs, double* traj, double* arc, double* smooth, double* min_dist,
+                          long long* n_viol);
+int st_solve_end(st_plan* plan, float* timings_ms);
+
 /* Page-locked host memory for output arrays (device-to-host copies at full link speed;
- * the Python binding pools these buffers for the report trajectories). */
+ * the Python binding pools these buffers for the report outputs). */
 int st_host_alloc(long long bytes, void** out);
 int st_host_free(void* ptr);
 

@@ -130,6 +130,7 @@ struct st_plan {
   std::vector<long long> lg_key;  // layout whose tables are in d_lgw
   std::map<std::vector<int>, Launch> launch_cache;  // choose_launch results (see choose_launch_cached)
   std::mutex mu;
+  bool async_pending = false;  // st_solve_report_begin enqueued, st_solve_end not yet called
 };
 
 namespace {
@@ -1169,13 +1170,15 @@ int st_solve_device(st_plan* pl, int batch, const double* c0, const double* beq,
 
 static int solve_host(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom, int switch_every,
              int max_iters, double tol, int flags, int hint, double* c_out, double* hist, int* iters, int* conv,
-             double* lam_out, double* d_out, float* timings, const ShardExt* ext, const ReportReq* rep = nullptr) {
+             double* lam_out, double* d_out, float* timings, const ShardExt* ext, const ReportReq* rep = nullptr,
+             bool async_ = false) {
   int rc = check_common(pl, batch, switch_every, max_iters, tol, flags);
   if (rc) return rc;
   if (!c0 || !beq || !geom || !c_out || !hist || !iters || !conv) return fail(ST_EINVAL, "NULL buffer");
   const bool keep = flags & ST_FLAG_KEEP_STATE;
   if (keep && (!lam_out || !d_out)) return fail(ST_EINVAL, "keep_state buffers missing");
   std::lock_guard<std::mutex> g(pl->mu);
+  if (pl->async_pending) return fail(ST_EINVAL, "a solve begun on this plan has not ended (st_solve_end)");
   ST_CUDA(cudaSetDevice(pl->device));
   const bool large = hint <= 0 && large_eligible(pl, batch, keep);
   Launch L;
@@ -1211,7 +1214,7 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
   // staging buffer, right after the solve inputs (a pageable copy would block the host)
   const bool rep_verdict = rep && (rep->min_dist || rep->n_viol);
   const size_t rep_in = rep_verdict ? (size_t)batch * 16 + (size_t)batch * pl->nobs * 40 : 0;
-  const bool staged = !keep && in_bytes + rep_in + small_out <= ((size_t)1 << 20);
+  const bool staged = !keep && !async_ && in_bytes + rep_in + small_out <= ((size_t)1 << 20);
   if (staged && in_bytes + rep_in + small_out > pl->stage_bytes) {
     if (pl->h_stage) cudaFreeHost(pl->h_stage);
     pl->h_stage = nullptr;
@@ -1242,7 +1245,7 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
                    keep ? d_lam : nullptr, keep ? d_dd : nullptr, s, ext);
   if (rc) return rc;
   ST_CUDA(cudaEventRecord(pl->ev[2], s));
-  std::vector<unsigned long long> mt;
+  bool verdict_out = false;
   const double* rep_small = nullptr;  // device: arc | smooth | min bits | counts (report pass)
   if (rep) {
     // report pass on the device: trajectories, arc length / smoothness, collision summary
@@ -1281,9 +1284,16 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     }
     ST_CUDA(swarm_report_launch(batch, n, m, nv, pl->nvmax, d_cout, pl->P, r_traj, r_arc, r_smooth, s));
     if (verdict) {
+      // r_mt: the minimum normalized distance's bits (non-negative doubles order as integers) |
+      // violation counts (64-bit) -- copied bit for bit into min_dist / n_viol
       ST_CUDA(swarm_collision_summary_launch(batch, n, m, r_traj, r_geom, n_obs, r_obs, r_cnt, r_mt, s));
-      mt.resize(2 * (size_t)batch);
-      if (!staged) ST_CUDA(cudaMemcpyAsync(mt.data(), r_mt, (size_t)batch * 16, cudaMemcpyDeviceToHost, s));
+      verdict_out = true;
+      if (!staged) {
+        if (rep->min_dist)
+          ST_CUDA(cudaMemcpyAsync(rep->min_dist, r_mt, (size_t)batch * 8, cudaMemcpyDeviceToHost, s));
+        if (rep->n_viol)
+          ST_CUDA(cudaMemcpyAsync(rep->n_viol, r_mt + batch, (size_t)batch * 8, cudaMemcpyDeviceToHost, s));
+      }
     }
     if (rep->traj) ST_CUDA(cudaMemcpyAsync(rep->traj, r_traj, (size_t)batch * n * m * 24, cudaMemcpyDeviceToHost, s));
     if (!staged) {
@@ -1309,6 +1319,10 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
     ST_CUDA(cudaMemcpyAsync(d_out, d_dd, n_d * 8, cudaMemcpyDeviceToHost, s));
   }
   ST_CUDA(cudaEventRecord(pl->ev[3], s));
+  if (async_) {  // st_solve_report_begin: every copy targets page-locked memory; st_solve_end waits
+    pl->async_pending = true;
+    return ST_OK;
+  }
   ST_CUDA(cudaStreamSynchronize(s));
   ST_CUDA(cudaGetLastError());
   if (timings) {
@@ -1326,15 +1340,10 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
       const char* r = o + out_small;
       if (rep->arc) memcpy(rep->arc, r, (size_t)batch * n * 8);
       if (rep->smooth) memcpy(rep->smooth, r + (size_t)batch * n * 8, (size_t)batch * n * 8);
-      if (!mt.empty()) memcpy(mt.data(), r + (size_t)batch * 2 * n * 8, (size_t)batch * 16);
-    }
-  }
-  if (rep && !mt.empty()) {
-    for (int b = 0; b < batch; ++b) {
-      double mn;
-      memcpy(&mn, &mt[b], 8);
-      if (rep->min_dist) rep->min_dist[b] = mn;
-      if (rep->n_viol) rep->n_viol[b] = (long long)mt[batch + b];
+      if (verdict_out) {
+        if (rep->min_dist) memcpy(rep->min_dist, r + (size_t)batch * 2 * n * 8, (size_t)batch * 8);
+        if (rep->n_viol) memcpy(rep->n_viol, r + (size_t)batch * (2 * n + 1) * 8, (size_t)batch * 8);
+      }
     }
   }
   return ST_OK;
@@ -1361,6 +1370,38 @@ int st_solve_report(st_plan* pl, int batch, const double* c0, const double* beq,
   const ReportReq rep{col_geom, col_obs, traj, arc, smooth, min_dist, n_viol};
   return solve_host(pl, batch, c0, beq, geom, switch_every, max_iters, tol, flags, hint, c_out, hist, iters, conv,
                     nullptr, nullptr, timings, nullptr, &rep);
+}
+
+int st_solve_report_begin(st_plan* pl, int batch, const double* c0, const double* beq, const double* geom,
+                          int switch_every, int max_iters, double tol, int flags, int hint, double* c_out,
+                          double* hist, int* iters, int* conv, const double* col_geom, const double* col_obs,
+                          double* traj, double* arc, double* smooth, double* min_dist, long long* n_viol) {
+  if (!pl) return fail(ST_EINVAL, "NULL plan");
+  if ((min_dist || n_viol) && (!col_geom || (pl->nobs > 0 && !col_obs)))
+    return fail(ST_EINVAL, "collision geometry missing");
+  if (batch > 65535) return fail(ST_EINVAL, "report pass: batch larger than 65535 scenarios");
+  if (pl->m < 1 || swarm_report_smem(pl->m) > (size_t)pl->smem_optin)
+    return fail(ST_EUNSUPPORTED, "report pass: too many samples per trajectory for one warp's shared memory");
+  if (flags & ST_FLAG_KEEP_STATE) return fail(ST_EINVAL, "report pass: keep_state solves use st_solve");
+  const ReportReq rep{col_geom, col_obs, traj, arc, smooth, min_dist, n_viol};
+  return solve_host(pl, batch, c0, beq, geom, switch_every, max_iters, tol, flags, hint, c_out, hist, iters, conv,
+                    nullptr, nullptr, nullptr, nullptr, &rep, true);
+}
+
+int st_solve_end(st_plan* pl, float* timings) {
+  if (!pl) return fail(ST_EINVAL, "NULL plan");
+  std::lock_guard<std::mutex> g(pl->mu);
+  if (!pl->async_pending) return fail(ST_EINVAL, "no solve begun on this plan");
+  pl->async_pending = false;
+  ST_CUDA(cudaSetDevice(pl->device));
+  ST_CUDA(cudaEventSynchronize(pl->ev[3]));
+  ST_CUDA(cudaGetLastError());
+  if (timings) {
+    ST_CUDA(cudaEventElapsedTime(&timings[0], pl->ev[0], pl->ev[1]));
+    ST_CUDA(cudaEventElapsedTime(&timings[1], pl->ev[1], pl->ev[2]));
+    ST_CUDA(cudaEventElapsedTime(&timings[2], pl->ev[2], pl->ev[3]));
+  }
+  return ST_OK;
 }
 
 // Page-locked host buffers (report outputs): device-to-host copies at full PCIe/C2C speed.

@@ -269,7 +269,8 @@ def boundary_arrays(specs) -> np.ndarray:
     return out.reshape(3, B, 2, n, 3).transpose(1, 2, 0, 3, 4)
 
 
-def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None, obs_rows: np.ndarray | None = None):
+def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None, obs_rows: np.ndarray | None = None,
+         alloc=np.empty):
     """Scenario batch -> (c0 (B,3,n,nv), b_eq (B,3,n,6), geom (B, 2+5 n_obs)).
 
     b_eq rows per agent and axis: [pos0, vel0, acc0, posT, velT, accT]
@@ -280,10 +281,12 @@ def pack(specs, basis: poly.Basis, bnd: np.ndarray | None = None, obs_rows: np.n
     n_obs = len(specs[0].obstacles)
     if bnd is None:
         bnd = boundary_arrays(specs)
-    beq = np.ascontiguousarray(bnd.transpose(0, 4, 3, 1, 2).reshape(B, 3, n, 6))
-    c0 = np.ascontiguousarray(poly.straight_line(basis, bnd[:, 0, 0].transpose(0, 2, 1),
-                                                 bnd[:, 1, 0].transpose(0, 2, 1)))
-    geom = np.empty((B, 2 + 5 * n_obs))
+    # alloc: the output arrays' allocator (page-locked buffers for the pipelined batch path)
+    beq = alloc((B, 3, n, 6))
+    np.copyto(beq.reshape(B, 3, n, 2, 3), bnd.transpose(0, 4, 3, 1, 2))
+    c0 = poly.straight_line(basis, bnd[:, 0, 0].transpose(0, 2, 1), bnd[:, 1, 0].transpose(0, 2, 1),
+                            out=alloc((B, 3, n, basis.num_coeffs)))
+    geom = alloc((B, 2 + 5 * n_obs))
     geom[:, :2] = [(spec.geometry.l_xy, spec.geometry.l_z) for spec in specs]
     if n_obs:
         if obs_rows is None:  # (B, n_obs, 5): centre, l_xy/2 + R, l_z/2 + R (problem.py:136-141)
@@ -534,9 +537,11 @@ def am_solve_batch(specs, config: SolverConfig | None = None, cache: kkt.FactorC
 
 
 # Large batches on the device report path run as a pipeline of contiguous chunks: while the
-# device solves chunk i (the ctypes call releases the GIL, a worker thread waits on it), the host
-# validates and packs chunk i+1 and builds the reports of chunk i-1.  Every scenario's result is
-# bitwise the one of the unchunked launch (same kernel and cluster shape; see tests).
+# device solves chunk i (enqueued by st_solve_report_begin, which returns at once), the host
+# validates and packs chunk i+1 and builds the reports of chunk i-1, then waits for chunk i with
+# st_solve_end.  (Libraries without the begin/end pair fall back to a worker thread that waits in
+# st_solve_report.)  Every scenario's result is bitwise the one of the unchunked launch (same
+# kernel and cluster shape; see tests).
 PIPELINE_MIN_BATCH = 256
 _POOL = None
 _POOL_LOCK = __import__("threading").Lock()
@@ -555,10 +560,29 @@ def _pipeline_chunks(B: int) -> int:
     env = __import__("os").environ.get("SWARM_PIPE_CHUNKS")
     if env is not None:
         return max(1, min(B, int(env)))
-    return 1 if B < PIPELINE_MIN_BATCH else 3
+    return 1 if B < PIPELINE_MIN_BATCH else 4
 
 
-def _prep_chunk(specs, basis, n_obs):
+def _chunk_bounds(B: int, K: int, limit: int = 65535) -> list:
+    """Chunk boundaries of a pipelined batch: the first chunk half the size of the others (the
+    device starts after packing it, the later chunks are packed while the device runs), none
+    larger than ``limit`` scenarios (one report-pass launch)."""
+    if K <= 1:
+        return [0, B]
+    while True:
+        w = [0.5] + [1.0] * (K - 1)
+        acc = np.cumsum([0.0] + w) / sum(w)
+        bounds = [int(B * x + 0.5) for x in acc]
+        sizes = [b - a for a, b in zip(bounds, bounds[1:])]
+        if min(sizes) < 1:
+            bounds = [B * i // K for i in range(K + 1)]  # tiny batches: equal chunks
+            sizes = [b - a for a, b in zip(bounds, bounds[1:])]
+        if max(sizes) <= limit or K >= B:
+            return bounds
+        K += 1
+
+
+def _prep_chunk(specs, basis, n_obs, alloc=np.empty):
     """Validation (raises before this chunk's device work) and packing of one chunk."""
     t0 = time.perf_counter()
     bnd = boundary_arrays(specs)
@@ -573,7 +597,7 @@ def _prep_chunk(specs, basis, n_obs):
         for v in validate_batch(specs, bnd[:, 0, 0], bnd[:, 1, 0], col_obs):
             if v:
                 raise _infeasible(v)
-    c0, beq, geom = pack(specs, basis, bnd, col_obs)
+    c0, beq, geom = pack(specs, basis, bnd, col_obs, alloc)
     col_geom = geom[:, :2]
     return t0, time.perf_counter(), c0, beq, geom, col_geom, col_obs
 
@@ -607,8 +631,13 @@ def _am_solve_batch(specs, config, cache, with_metrics) -> list:
     report_path = (not config.keep_state and 3 <= basis.num_samples <= 2000 and native.load().swarm_has_report)
     B = len(specs)
     K = max(_pipeline_chunks(B), -(-B // 65535)) if report_path else 1
-    bounds = [B * i // K for i in range(K + 1)]
-    prep = _prep_chunk(specs[: bounds[1]], basis, n_obs)
+    bounds = _chunk_bounds(B, K)
+    K = len(bounds) - 1
+    # the pipelined path enqueues each chunk and returns (st_solve_report_begin): its inputs are
+    # packed straight into page-locked buffers so the copies run asynchronously
+    pipelined = K > 1 and native.load().swarm_has_async
+    alloc = native.pinned_empty if pipelined else np.empty
+    prep = _prep_chunk(specs[: bounds[1]], basis, n_obs, alloc)
     fp = kkt.fingerprint(basis, n, n_obs)
     cache, foreign = _resolve_cache(cache)
     schedule = config.schedule()
@@ -635,9 +664,43 @@ def _am_solve_batch(specs, config, cache, with_metrics) -> list:
         return _make_reports(specs[bounds[i]: bounds[i + 1]], out, basis, plan, cache, schedule, config,
                              (pr[0], pr[1], t2, t3), with_metrics, foreign=foreign)
 
+    def begin(pr):
+        _, _, c0, beq, geom, col_geom, col_obs = pr
+        t2 = time.perf_counter()
+        pend = plan.solve_report_begin(c0, beq, geom, schedule.switch_every, config.max_iters, config.tolerance,
+                                       col_geom, col_obs, cluster_hint=hint, fp32=fp32, with_metrics=with_metrics)
+        return pend, t2
+
+    def end(started):
+        pend, t2 = started
+        out = pend.end()
+        return out, t2, time.perf_counter()
+
     if K == 1:
         res = solve(prep)
         reports = finish(0, prep, res)
+    elif pipelined:
+        # the device solves chunk i while this thread packs chunk i+1 and builds the reports of
+        # chunk i-1: the library enqueues a chunk and returns (st_solve_report_begin), and
+        # st_solve_end waits for it, so no Python thread has to win the GIL back to keep the
+        # device fed
+        reports = []
+        started = begin(prep)
+        for i in range(1, K):
+            try:
+                nxt = _prep_chunk(specs[bounds[i]: bounds[i + 1]], basis, n_obs, alloc)
+            except BaseException:
+                end(started)  # no solve left pending on the plan when the error propagates
+                raise
+            res = end(started)
+            started = begin(nxt)
+            try:
+                reports += finish(i - 1, prep, res)
+            except BaseException:
+                end(started)
+                raise
+            prep = nxt
+        reports += finish(K - 1, prep, end(started))
     else:
         pool = _solver_thread()
         reports = []

@@ -28,7 +28,8 @@ _ERRORS = {1: ValueError, 2: RuntimeError, 3: MemoryError, 4: NotImplementedErro
 EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_report", "st_solve_device", "st_query_launch",
            "st_last_error", "st_version", "st_shard_layout", "st_shard_buffer", "st_shard_open", "st_shard_close",
            "st_shard_reset", "st_solve_sharded", "st_check_collisions",
-           "st_check_collisions_batch", "st_large_partition", "st_host_alloc", "st_host_free")
+           "st_check_collisions_batch", "st_large_partition", "st_host_alloc", "st_host_free",
+           "st_solve_report_begin", "st_solve_end")
 
 _lib = None
 _lock = threading.Lock()
@@ -57,11 +58,16 @@ def load() -> ctypes.CDLL:
         optional = set()
         if os.environ.get("SWARM_LIB"):
             # A/B runs against an older build of the library: entries it lacks are optional
-            optional = {nm for nm in ("st_solve_report", "st_host_alloc", "st_host_free") if not hasattr(lib, nm)}
+            optional = {nm for nm in ("st_solve_report", "st_host_alloc", "st_host_free", "st_solve_report_begin",
+                                      "st_solve_end") if not hasattr(lib, nm)}
         if "st_solve_report" not in optional:
             lib.st_solve_report.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip,
                                             ctypes.POINTER(ctypes.c_float), _dp, _dp, _dp, _dp, _dp, _dp,
                                             ctypes.POINTER(ctypes.c_longlong)]
+        if "st_solve_report_begin" not in optional:
+            lib.st_solve_report_begin.argtypes = [vp, i, _dp, _dp, _dp, i, i, d, i, i, _dp, _dp, _ip, _ip, _dp, _dp,
+                                                  _dp, _dp, _dp, _dp, ctypes.POINTER(ctypes.c_longlong)]
+            lib.st_solve_end.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
         lib.st_query_launch.argtypes = [vp, i, i, i, ctypes.POINTER(ctypes.c_longlong)]
         lib.st_last_error.restype = ctypes.c_char_p
         ub = ctypes.POINTER(ctypes.c_ubyte)
@@ -84,6 +90,7 @@ def load() -> ctypes.CDLL:
             if name not in optional:
                 getattr(lib, name)  # every declared symbol must resolve
         lib.swarm_has_report = "st_solve_report" not in optional
+        lib.swarm_has_async = "st_solve_report_begin" not in optional and "st_host_alloc" not in optional
         _lib = lib
         return lib
 
@@ -113,9 +120,10 @@ class _PinnedPool:
         self._lock = threading.Lock()
         self._keep = keep
 
-    def empty(self, shape) -> np.ndarray:
+    def empty(self, shape, dtype=np.float64) -> np.ndarray:
+        dtype = np.dtype(dtype)
         count = int(np.prod(shape))
-        nbytes = max(8, count * 8)
+        nbytes = max(8, count * dtype.itemsize)
         with self._lock:
             bucket = self._free.get(nbytes)
             ptr = bucket.pop() if bucket else None
@@ -125,7 +133,7 @@ class _PinnedPool:
             ptr = p.value
         raw = (ctypes.c_byte * nbytes).from_address(ptr)
         weakref.finalize(raw, self._release, ptr, nbytes)
-        return np.frombuffer(raw, dtype=np.float64, count=count).reshape(shape)
+        return np.frombuffer(raw, dtype=dtype, count=count).reshape(shape)
 
     def _release(self, ptr: int, nbytes: int) -> None:
         with self._lock:
@@ -140,6 +148,11 @@ class _PinnedPool:
 
 
 _PINNED = _PinnedPool()
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """An uninitialized page-locked host array (pooled buffer, returned when the array dies)."""
+    return _PINNED.empty(shape, dtype)
 
 
 class Plan:
@@ -259,6 +272,36 @@ class Plan:
             res.update(arc=arc, smooth=smooth, min_dist=mind, n_viol=nviol)
         return res
 
+    def solve_report_begin(self, c0, beq, geom, switch_every: int, max_iters: int, tol: float, col_geom, col_obs,
+                           cluster_hint: int = 0, fp32: bool = False, with_metrics: bool = True) -> "PendingSolve":
+        """First half of ``solve_report`` (``st_solve_report_begin``): the inputs are copied and the
+        solve, report pass and output copies (into page-locked arrays) are enqueued; ``end()`` on
+        the returned object waits and gives ``solve_report``'s dict.  Nothing else may use this
+        plan from the host in between (the library refuses)."""
+        c0 = np.ascontiguousarray(c0, dtype=np.float64)
+        beq = np.ascontiguousarray(beq, dtype=np.float64)
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        col_geom = np.ascontiguousarray(col_geom, dtype=np.float64)
+        col_obs = np.ascontiguousarray(col_obs, dtype=np.float64)
+        B = c0.shape[0]
+        if c0.shape != (B, 3, self.n, self.nv) or beq.shape != (B, 3, self.n, 6) or \
+                geom.shape != (B, 2 + 5 * self.n_obs) or col_geom.shape != (B, 2) or \
+                col_obs.shape != (B, self.n_obs, 5):
+            raise ValueError("batch arrays do not match the plan's shape")
+        out = {"c": _PINNED.empty(c0.shape), "hist": _PINNED.empty((B, 3, max_iters)),
+               "iters": _PINNED.empty((B,), np.int32), "status": _PINNED.empty((B,), np.int32),
+               "traj": _PINNED.empty((B, self.n, self.m, 3))}
+        if with_metrics:
+            out.update(arc=_PINNED.empty((B, self.n)), smooth=_PINNED.empty((B, self.n)),
+                       min_dist=_PINNED.empty((B,)), n_viol=_PINNED.empty((B,), np.int64))
+        g = out.get
+        _check(self._lib.st_solve_report_begin(
+            self._h, B, _ptr(c0), _ptr(beq), _ptr(geom), switch_every, max_iters, tol, ST_FLAG_FP32 if fp32 else 0,
+            cluster_hint, _ptr(out["c"]), _ptr(out["hist"]), _ptr(out["iters"], _ip), _ptr(out["status"], _ip),
+            _ptr(col_geom), _ptr(col_obs), _ptr(out["traj"]), _ptr(g("arc")), _ptr(g("smooth")), _ptr(g("min_dist")),
+            _ptr(g("n_viol"), ctypes.POINTER(ctypes.c_longlong))))
+        return PendingSolve(self, out)
+
     def solve_device(self, B: int, c0_ptr: int, beq_ptr: int, geom_ptr: int, switch_every: int,
                      max_iters: int, tol: float, c_out_ptr: int, hist_ptr: int, iters_ptr: int,
                      conv_ptr: int, stream: int = 0, cluster_hint: int = 0, fp32: bool = False) -> None:
@@ -309,6 +352,24 @@ class Plan:
                                           t))
         return {"c": c_out, "hist": hist, "iters": iters, "converged": conv.astype(bool),
                 "timings_ms": tuple(float(x) for x in t)}
+
+
+class PendingSolve:
+    """A solve begun with ``Plan.solve_report_begin``; ``end()`` waits for it (once)."""
+
+    def __init__(self, plan: Plan, out: dict):
+        self._plan, self._out = plan, out
+
+    def end(self) -> dict:
+        plan, out = self._plan, self._out
+        if plan is None:
+            raise RuntimeError("solve already ended")
+        self._plan = None
+        t = (ctypes.c_float * 3)()
+        _check(plan._lib.st_solve_end(plan._h, t))
+        out["converged"] = out["status"] > 0
+        out.update(lam=None, d=None, timings_ms=tuple(float(x) for x in t))
+        return out
 
 
 def check_collisions(traj: np.ndarray, l_xy: float, l_z: float, obs_rows: np.ndarray, device: int = 0,

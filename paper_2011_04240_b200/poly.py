@@ -113,20 +113,23 @@ def endpoint_rows(basis: Basis) -> np.ndarray:
                       basis.P[-1], basis.Pdot[-1], basis.Pddot[-1]])
 
 
-def straight_line(basis: Basis, start: np.ndarray, goal: np.ndarray) -> np.ndarray:
+def straight_line(basis: Basis, start: np.ndarray, goal: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
     """Straight-line coefficients for many scalars at once: (...,) x2 -> (..., n_v).
 
-    Bernstein: c_k = s + (k/d)(g - s); monomial: [s, g - s, 0, ...].
+    Bernstein: c_k = s + (k/d)(g - s); monomial: [s, g - s, 0, ...].  ``out``: optional
+    C-contiguous destination of that shape (e.g. a page-locked buffer).
     """
     start = np.asarray(start, dtype=float)
     goal = np.asarray(goal, dtype=float)
     nv = basis.num_coeffs
+    if out is None:
+        out = np.empty(start.shape + (nv,))
     if basis.kind == BasisKind.BERNSTEIN:
         frac = np.arange(nv) / basis.degree
-        out = np.multiply.outer(np.subtract(goal, start, order="C"), frac)  # = s + frac (g - s), bitwise
+        np.multiply.outer(np.subtract(goal, start, order="C"), frac, out=out)  # = s + frac (g - s), bitwise
         out += start[..., None]
         return out
-    out = np.zeros(start.shape + (nv,))
+    out[...] = 0.0
     out[..., 0] = start
     out[..., 1] = goal - start
     return out

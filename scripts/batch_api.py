@@ -14,7 +14,9 @@ for chunks in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["1", "2", "3", 
     os.environ["SWARM_PIPE_CHUNKS"] = chunks
     for with_metrics in (False, True):
         best = 1e9
+        reps = None
         for _ in range(3):
+            reps = None  # free the previous reports outside the timed region
             t = time.perf_counter()
             reps = am_solve_batch(specs, cache=cache, with_metrics=with_metrics)
             best = min(best, time.perf_counter() - t)

@@ -45,7 +45,7 @@ def test_report_pass_matches_host_formulas(cuda_ok, obstacles):
 
 @pytest.mark.gpu
 def test_pipelined_batch_is_bitwise_the_single_launch(cuda_ok, monkeypatch):
-    from paper_2011_04240_b200 import am_solve_batch
+    from paper_2011_04240_b200 import am_solve_batch, engine
     specs = _specs(300)
     monkeypatch.setenv("SWARM_PIPE_CHUNKS", "1")
     one = am_solve_batch(specs)
@@ -53,7 +53,9 @@ def test_pipelined_batch_is_bitwise_the_single_launch(cuda_ok, monkeypatch):
     three = am_solve_batch(specs)
     monkeypatch.setenv("SWARM_PIPE_CHUNKS", "7")
     seven = am_solve_batch(specs, with_metrics=False)
-    assert {r.timings["batch"] for r in three} == {100}
+    b3 = engine._chunk_bounds(300, 3)
+    assert b3 == [0, 60, 180, 300]  # first chunk half the others
+    assert [r.timings["batch"] for r in three] == [b - a for a, b in zip(b3, b3[1:]) for _ in range(b - a)]
     for a, b, c in zip(one, three, seven):
         assert a.iterations == b.iterations == c.iterations
         assert np.array_equal(a.coefficients, b.coefficients) and np.array_equal(a.coefficients, c.coefficients)
@@ -84,9 +86,14 @@ def test_pipeline_chunking_rule(monkeypatch):
     from paper_2011_04240_b200 import engine
     monkeypatch.delenv("SWARM_PIPE_CHUNKS", raising=False)
     assert engine._pipeline_chunks(1) == 1 and engine._pipeline_chunks(255) == 1
-    assert engine._pipeline_chunks(1024) == 3
+    assert engine._pipeline_chunks(1024) == 4
     monkeypatch.setenv("SWARM_PIPE_CHUNKS", "5")
     assert engine._pipeline_chunks(3) == 3 and engine._pipeline_chunks(100) == 5
+    # chunk bounds: first chunk half the others, every chunk within one report launch
+    for B, K in ((1024, 3), (7, 7), (300, 4), (200000, 3)):
+        b = engine._chunk_bounds(B, K)
+        sizes = [y - x for x, y in zip(b, b[1:])]
+        assert b[0] == 0 and b[-1] == B and min(sizes) >= 1 and max(sizes) <= 65535 and len(b) - 1 >= K
 
 
 @pytest.mark.gpu

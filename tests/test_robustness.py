@@ -35,8 +35,8 @@ def test_nan_state_raises_through_am_solve(cuda_ok, monkeypatch):
     spec = generate_random(8, (8.0, 8.0, 3.0), 0.4, 0)
     real_pack = engine.pack
 
-    def poisoned(specs, basis, bnd=None, obs_rows=None):
-        c0, beq, geom = real_pack(specs, basis, bnd, obs_rows)
+    def poisoned(specs, basis, *args):
+        c0, beq, geom = real_pack(specs, basis, *args)
         c0[0, 0, 0, 5] = np.inf
         return c0, beq, geom
 
