@@ -86,10 +86,10 @@ int swarm_fail(int code, const std::string& msg) { return fail(code, msg); }
 // report.cu / collisions.cu: the device-side report pass of st_solve_report
 size_t swarm_report_smem(int m);
 cudaError_t swarm_report_launch(int B, int n, int m, int nv, int nvp, const double* c, const double* P, double* traj,
-                                double* arc, double* smooth, cudaStream_t s);
+                                double* arc, double* smooth, unsigned long long* summary, cudaStream_t s);
 cudaError_t swarm_collision_summary_launch(int B, int n, int m, const double* d_traj, const double* d_geom, int n_obs,
                                            const double* d_obs, int* row_cnt, unsigned long long* min_total,
-                                           cudaStream_t s);
+                                           cudaStream_t s, bool init = true);
 
 // outputs of the report pass (st_solve_report); any output may be NULL
 struct ReportReq {
@@ -1282,11 +1282,12 @@ static int solve_host(st_plan* pl, int batch, const double* c0, const double* be
         ST_CUDA(cudaMemcpyAsync(r_obs, staged ? g2 + (size_t)batch * 16 : (const char*)rep->obs,
                                 (size_t)batch * n_obs * 40, cudaMemcpyHostToDevice, s));
     }
-    ST_CUDA(swarm_report_launch(batch, n, m, nv, pl->nvmax, d_cout, pl->P, r_traj, r_arc, r_smooth, s));
+    ST_CUDA(swarm_report_launch(batch, n, m, nv, pl->nvmax, d_cout, pl->P, r_traj, r_arc, r_smooth,
+                                verdict ? r_mt : nullptr, s));
     if (verdict) {
       // r_mt: the minimum normalized distance's bits (non-negative doubles order as integers) |
       // violation counts (64-bit) -- copied bit for bit into min_dist / n_viol
-      ST_CUDA(swarm_collision_summary_launch(batch, n, m, r_traj, r_geom, n_obs, r_obs, r_cnt, r_mt, s));
+      ST_CUDA(swarm_collision_summary_launch(batch, n, m, r_traj, r_geom, n_obs, r_obs, r_cnt, r_mt, s, false));
       verdict_out = true;
       if (!staged) {
         if (rep->min_dist)

@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) rows_kernel(Rows R, int* 
   const RowGeom g = row_geom(R, scn, row);
   double vmin = INFINITY;
   int cnt = 0;
-  for (int r0 = 0; r0 < R.m; r0 += 32) {
+#pragma unroll 4
+  for (int r0 = 0; r0 < R.m; r0 += 32) {  // independent sample chunks: loads of several in flight
     const int r = r0 + lane;
     double v = r < R.m ? row_value(g, r) : INFINITY;
     vmin = fmin(vmin, v);  // a NaN never lowers the minimum (Python's min(minimum, nan) keeps minimum)
@@ -241,9 +242,9 @@ __global__ void init_summary_kernel(unsigned long long* min_total, int B) {
 // B x n x m x 3 trajectories already on the device; row_cnt: B x n_rows scratch.
 cudaError_t swarm_collision_summary_launch(int B, int n, int m, const double* d_traj, const double* d_geom, int n_obs,
                                            const double* d_obs, int* row_cnt, unsigned long long* min_total,
-                                           cudaStream_t s) {
+                                           cudaStream_t s, bool init) {
   if (B <= 0) return cudaSuccess;
-  init_summary_kernel<<<(B + 255) / 256, 256, 0, s>>>(min_total, B);
+  if (init) init_summary_kernel<<<(B + 255) / 256, 256, 0, s>>>(min_total, B);  // else: set by the report pass
   const long long n_pairs = (long long)n * (n - 1) / 2, n_rows = n_pairs + (long long)n * n_obs;
   if (n_rows == 0 || m == 0) return cudaGetLastError();
   Rows R{d_traj, d_obs, d_geom, n, m, n_obs, n_pairs, n_rows};

@@ -20,28 +20,43 @@ namespace {
 
 constexpr int kWarps = 4;
 
+constexpr int kMaxCoeffs = 16;  // n_v <= 16 (st_plan_create)
+
 __global__ void __launch_bounds__(kWarps * 32) report_kernel(int B, int n, int m, int nv, int nvp, const double* c,
                                                              const double* P, double* traj, double* arc,
-                                                             double* smooth) {
+                                                             double* smooth, unsigned long long* summary) {
   extern __shared__ double xs[];  // kWarps x m x 3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long agent = (long long)blockIdx.x * kWarps + warp;  // b * n + j
   if (agent >= (long long)B * n) return;
   const long long b = agent / n, j = agent - b * n;
+  if (summary && j == 0 && lane == 0) {  // the collision summary's initial values (rows_kernel runs after)
+    summary[b] = 0x7ff0000000000000ULL;  // +inf bits
+    summary[B + b] = 0;
+  }
   double* x = xs + (size_t)warp * m * 3;
   const double* cb = c + (size_t)b * 3 * n * nv;
-  const double* cx = cb + (size_t)j * nv;
-  const double* cy = cb + ((size_t)n + j) * nv;
-  const double* cz = cb + ((size_t)2 * n + j) * nv;
+  double cx[kMaxCoeffs], cy[kMaxCoeffs], cz[kMaxCoeffs];  // the agent's coefficient rows, in registers
+#pragma unroll
+  for (int k = 0; k < kMaxCoeffs; ++k) {
+    cx[k] = k < nv ? cb[(size_t)j * nv + k] : 0.0;
+    cy[k] = k < nv ? cb[((size_t)n + j) * nv + k] : 0.0;
+    cz[k] = k < nv ? cb[((size_t)2 * n + j) * nv + k] : 0.0;
+  }
   double* out = traj + (size_t)agent * m * 3;
   for (int t = lane; t < m; t += 32) {
     const double* pr = P + (size_t)t * nvp;
+    double pk[kMaxCoeffs];
+#pragma unroll
+    for (int k = 0; k < kMaxCoeffs; ++k) pk[k] = k < nv ? pr[k] : 0.0;  // all loads in flight at once
     double vx = 0.0, vy = 0.0, vz = 0.0;
-    for (int k = 0; k < nv; ++k) {
-      const double pk = pr[k];
-      vx = fma(cx[k], pk, vx);
-      vy = fma(cy[k], pk, vy);
-      vz = fma(cz[k], pk, vz);
+#pragma unroll
+    for (int k = 0; k < kMaxCoeffs; ++k) {
+      if (k < nv) {  // k-ascending FMA chains, as before
+        vx = fma(cx[k], pk[k], vx);
+        vy = fma(cy[k], pk[k], vy);
+        vz = fma(cz[k], pk[k], vz);
+      }
     }
     x[3 * t] = vx;
     x[3 * t + 1] = vy;
@@ -80,8 +95,10 @@ __global__ void __launch_bounds__(kWarps * 32) report_kernel(int B, int n, int m
 size_t swarm_report_smem(int m) { return (size_t)kWarps * m * 3 * sizeof(double); }
 
 // c: B x 3 x n x nv (device), P: m x nvp (device, zero-padded rows); outputs on the device.
+// summary (optional, B x 2 words): set to the collision summary's initial values (+inf bits, 0)
+// for swarm_collision_summary_launch(..., init = false) to accumulate into.
 cudaError_t swarm_report_launch(int B, int n, int m, int nv, int nvp, const double* c, const double* P, double* traj,
-                                double* arc, double* smooth, cudaStream_t s) {
+                                double* arc, double* smooth, unsigned long long* summary, cudaStream_t s) {
   const long long agents = (long long)B * n;
   if (agents == 0 || m == 0) return cudaSuccess;
   const size_t smem = swarm_report_smem(m);
@@ -90,6 +107,6 @@ cudaError_t swarm_report_launch(int B, int n, int m, int nv, int nvp, const doub
     if (e != cudaSuccess) return e;
   }
   report_kernel<<<(unsigned)((agents + kWarps - 1) / kWarps), kWarps * 32, smem, s>>>(B, n, m, nv, nvp, c, P, traj,
-                                                                                       arc, smooth);
+                                                                                       arc, smooth, summary);
   return cudaGetLastError();
 }
