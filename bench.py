@@ -259,12 +259,15 @@ def single_solve_ms(names=("circ16j", "rand32_s0", "hall16j", "sph64j", "rand128
             if not fp32:
                 n = len(spec.start)
                 ps = _pair_samples(spec, r.iterations)
-                large = n > 64
+                large = n > 64  # roofline: the multiplier stream (HBM) vs the FP64 pair arithmetic
                 bytes_ = BYTES_PER_PAIR_SAMPLE * ps
                 flops = FLOP_PER_PAIR_SAMPLE * ps
+                # the library's rule (capi.cu large_eligible): obstacle-free single solves above 32 agents
+                # run on the whole-GPU large-fleet kernel
+                large_kernel = n > 32 and not spec.obstacles
                 row.update({"ms": round(best, 4), "iterations": r.iterations, "converged": r.converged,
                             "end_to_end_ms": round(r.timings["total_s"] * 1e3, 3),
-                            "kernel": "am_large_kernel" if large else "am_cluster_kernel"})
+                            "kernel": "am_large_kernel" if large_kernel else "am_cluster_kernel"})
                 if large:
                     gbs = bytes_ / (best / 1e3) / 1e9
                     row["roofline"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
