@@ -72,7 +72,11 @@ def sample_seeds(count: int) -> list[int]:
 
 
 def _cpu_worker(seeds):
+    # one BLAS thread per worker process (one process per core): numpy may already be loaded in
+    # the spawned child, so the limit is set at run time as well as through the environment
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
     from scipy.linalg import lu_factor
 
     from oracle import am_oracle
