@@ -210,7 +210,12 @@ FLOP_PER_PAIR_SAMPLE_F = FLOP_PER_PAIR_SAMPLE
 def _cpu_single(name: str, max_iters: int | None = None):
     """Same-run CPU time of the reference algorithm (oracle port, numpy/scipy LU, 1 thread, warm
     factors): best of 3 for full solves, or the mean per-iteration time of a bounded prefix."""
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):  # numpy is loaded in this process already: limit BLAS at run time
+        return _cpu_single_1t(name, max_iters)
+
+
+def _cpu_single_1t(name: str, max_iters: int | None):
     from scipy.linalg import lu_factor
 
     from oracle import am_oracle
