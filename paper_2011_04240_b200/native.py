@@ -300,7 +300,7 @@ class Plan:
             cluster_hint, _ptr(out["c"]), _ptr(out["hist"]), _ptr(out["iters"], _ip), _ptr(out["status"], _ip),
             _ptr(col_geom), _ptr(col_obs), _ptr(out["traj"]), _ptr(g("arc")), _ptr(g("smooth")), _ptr(g("min_dist")),
             _ptr(g("n_viol"), ctypes.POINTER(ctypes.c_longlong))))
-        return PendingSolve(self, out)
+        return PendingSolve(self, out, (c0, beq, geom, col_geom, col_obs))
 
     def solve_device(self, B: int, c0_ptr: int, beq_ptr: int, geom_ptr: int, switch_every: int,
                      max_iters: int, tol: float, c_out_ptr: int, hist_ptr: int, iters_ptr: int,
@@ -355,10 +355,13 @@ class Plan:
 
 
 class PendingSolve:
-    """A solve begun with ``Plan.solve_report_begin``; ``end()`` waits for it (once)."""
+    """A solve begun with ``Plan.solve_report_begin``; ``end()`` waits for it (once).  The input
+    arrays are held until then (page-locked inputs are copied asynchronously); a pending solve
+    that is dropped without ``end()`` is ended by the finalizer, so the plan is never left
+    refusing calls."""
 
-    def __init__(self, plan: Plan, out: dict):
-        self._plan, self._out = plan, out
+    def __init__(self, plan: Plan, out: dict, inputs: tuple):
+        self._plan, self._out, self._inputs = plan, out, inputs
 
     def end(self) -> dict:
         plan, out = self._plan, self._out
@@ -366,10 +369,21 @@ class PendingSolve:
             raise RuntimeError("solve already ended")
         self._plan = None
         t = (ctypes.c_float * 3)()
-        _check(plan._lib.st_solve_end(plan._h, t))
+        try:
+            _check(plan._lib.st_solve_end(plan._h, t))
+        finally:
+            self._inputs = None
         out["converged"] = out["status"] > 0
         out.update(lam=None, d=None, timings_ms=tuple(float(x) for x in t))
         return out
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and getattr(plan, "_h", None):
+            try:
+                plan._lib.st_solve_end(plan._h, None)
+            except Exception:
+                pass
 
 
 def check_collisions(traj: np.ndarray, l_xy: float, l_z: float, obs_rows: np.ndarray, device: int = 0,

@@ -112,3 +112,36 @@ def test_pooled_trajectory_buffers_are_never_shared_with_live_reports(cuda_ok):
     for r, t in zip(a, keep):
         assert np.array_equal(r.trajectories, t)
     assert not any(np.shares_memory(x.trajectories, y.trajectories) for x in a for y in b)
+
+
+@pytest.mark.gpu
+def test_begin_end_equals_one_call_and_guards_the_plan(cuda_ok):
+    """st_solve_report_begin / st_solve_end: the same outputs as st_solve_report, page-locked
+    outputs, other host-pointer calls on the plan refused while a solve is pending, and a
+    pending solve dropped without end() does not leave the plan refusing calls."""
+    import gc
+
+    from paper_2011_04240_b200 import SolverConfig, engine, kkt, poly
+    specs = _specs(20, n=16, obstacles=2)
+    basis = poly.for_spec(specs[0])
+    cfg = SolverConfig()
+    sch = cfg.schedule()
+    cache = kkt.FactorCache()
+    plan = engine._plan_for(cache, kkt.fingerprint(basis, 16, 2), basis, sch, 16, 2, 0)
+    _, _, c0, beq, geom, cg, co = engine._prep_chunk(specs, basis, 2)
+    args = (c0, beq, geom, sch.switch_every, cfg.max_iters, cfg.tolerance, cg, co)
+    one = plan.solve_report(*args)
+    pend = plan.solve_report_begin(*args)
+    with pytest.raises(ValueError, match="not ended"):
+        plan.solve_report(*args)
+    two = pend.end()
+    for k in ("c", "hist", "iters", "traj", "arc", "smooth", "min_dist", "n_viol"):
+        assert np.array_equal(one[k], two[k]), k
+    assert np.array_equal(one["converged"], two["converged"])
+    with pytest.raises(RuntimeError):
+        pend.end()
+    pend = plan.solve_report_begin(*args)
+    del pend
+    gc.collect()
+    three = plan.solve_report(*args)  # the finalizer ended the dropped solve
+    assert np.array_equal(one["c"], three["c"])
