@@ -145,3 +145,20 @@ def test_begin_end_equals_one_call_and_guards_the_plan(cuda_ok):
     gc.collect()
     three = plan.solve_report(*args)  # the finalizer ended the dropped solve
     assert np.array_equal(one["c"], three["c"])
+
+
+@pytest.mark.gpu
+def test_pipelined_obstacle_batch_is_bitwise_the_single_launch(cuda_ok, monkeypatch):
+    """The begin/end pipeline with obstacle rows (collision inputs staged per chunk) and FP32."""
+    from paper_2011_04240_b200 import SolverConfig, am_solve_batch
+    specs = _specs(260, n=8, obstacles=3)
+    for cfg in (SolverConfig(), SolverConfig(fp32=True)):
+        monkeypatch.setenv("SWARM_PIPE_CHUNKS", "1")
+        one = am_solve_batch(specs, cfg)
+        monkeypatch.setenv("SWARM_PIPE_CHUNKS", "4")
+        four = am_solve_batch(specs, cfg)
+        for a, b in zip(one, four):
+            assert a.iterations == b.iterations and a.converged == b.converged
+            assert np.array_equal(a.coefficients, b.coefficients)
+            assert np.array_equal(a.trajectories, b.trajectories)
+            assert a.metrics == b.metrics
