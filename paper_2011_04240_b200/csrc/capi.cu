@@ -216,7 +216,7 @@ long long layout(st_plan* pl, Launch& L, int C) {
   take(k.o_beq, 18LL * L.own_max);
   take(k.o_bb, 18);
   take(k.o_wp, 2LL * NW);
-  take(k.o_misc, 2);
+  take(k.o_misc, swarm::MI_INTS / 2);  // scenario slot | launch-constant index table (am_kernel.cuh)
   take(k.o_bnd, 2);
   k.o_lam = (int)o;
   L.lam_per_cta = (long long)L.tasks_max * L.nsteps * 96;
