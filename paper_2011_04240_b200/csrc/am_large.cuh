@@ -113,8 +113,15 @@ __device__ __forceinline__ LgCtx lg_ctx(const LgParams& p) {
 }
 
 struct LgSmem {  // byte offsets into dynamic shared memory
-  int ring, bar, xs, P, mat, blist, bbar, misc, total;
+  int ring, bar, xs, P, mat, blist, bbar, misc, rows, total;
 };
+
+// Launch-constant row indices of the R phase (ints at LgSmem::rows), filled once per launch so
+// that no per-iteration loop divides by a run-time value: header r_lo, r_hi, nr, LG_NT / nr,
+// LG_NT % nr; per thread its first (t, row) of the t-major (sample, row) loops as t << 16 | rl;
+// per row rl of this CTA (r = r_lo + rl) its axis and agent as ax << 16 | j.
+constexpr int LG_ROWS_MAX = 3 * 32 * LG_MAXB;  // 3 n rows at n = 256
+constexpr int LG_RT_START = 8, LG_RT_ROW = LG_RT_START + LG_NT;
 
 template <int NVMAX, bool F32>
 __host__ __device__ inline LgSmem lg_smem(int m, int chunk_rows) {
@@ -130,6 +137,7 @@ __host__ __device__ inline LgSmem lg_smem(int m, int chunk_rows) {
   s.blist = take(LG_MAXB * LG_MAXB * 4 + (LG_MAXB * (LG_MAXB + 1) / 2 + 1) * 4);
   s.bbar = take(18 * 8);
   s.misc = take(8 * 8 + LG_MAXB * 4);  // broadcast words + per-block seen epochs
+  s.rows = take((LG_RT_ROW + LG_ROWS_MAX) * 4);  // R-phase row indices (see LG_RT_*)
   s.total = o;
   return s;
 }
@@ -515,9 +523,11 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
   const double* mat = reinterpret_cast<const double*>(smb + L.mat);
   const int* blist = reinterpret_cast<const int*>(smb + L.blist);
   const double* bbar = reinterpret_cast<const double*>(smb + L.bbar);
-  const int n = p.n, m = p.m, R3 = 3 * n;
-  const int r_lo = (int)((long long)cx.cta * R3 / p.cpg), r_hi = (int)((long long)(cx.cta + 1) * R3 / p.cpg);
-  const int nr = r_hi - r_lo;
+  const int n = p.n, m = p.m;
+  const int* rt = reinterpret_cast<const int*>(smb + L.rows);
+  const int r_lo = rt[0], nr = rt[2], dt = rt[3], drl = rt[4];
+  const int* rowt = rt + LG_RT_ROW;  // ax << 16 | j per row of this CTA
+  const int start = rt[LG_RT_START + threadIdx.x];
   const int mt_n = (nr + 7) >> 3, rp = mt_n * 8;  // row tiles of the projection
   const long long xstride = 3LL * n * NVMAX + 4;
   // scratch in the multiplier ring (idle in this phase): q rows | warp partials | R | c
@@ -526,13 +536,13 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
   double* Rr = part + (size_t)LG_NW * rp * NH * 8;        // nr x NVMAX
   double* cr = Rr + (size_t)rp * NVMAX;                   // nr x NVMAX
   if (mode == 1 || mode == 2) {
+    int t = start >> 16, rl = start & 0xffff;  // idx = t * nr + rl, stepped without division
     for (int idx = threadIdx.x; idx < nr * m; idx += LG_NT) {
       // consecutive threads: consecutive rows (agents) at one t -> the slot loads coalesce
-      const int t = idx / nr, rl = idx - t * nr;
       double qv = 0.0;
       {
-        const int r = r_lo + rl;
-        const int ax = r / n, j = r - ax * n;
+        const int axj = rowt[rl];
+        const int ax = axj >> 16, j = axj & 0xffff;
         const int b = j >> 5, l = j & 31;
         const double* qb = p.qbuf + (k & 1) * p.q_stride + ax * 32 + l;  // written by pass k
         double v[2 * LG_MAXB];
@@ -551,6 +561,12 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
         for (int e = 0; e < 2 * LG_MAXB; ++e) qv += v[e];
       }
       qs[rl * m + t] = qv;
+      t += dt;
+      rl += drl;
+      if (rl >= nr) {
+        rl -= nr;
+        ++t;
+      }
     }
     __syncthreads();
     stamp(tsr, 8);
@@ -609,8 +625,8 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
     const double rho = mat[SM::RHO];
     for (int idx = threadIdx.x; idx < nr * NVMAX; idx += LG_NT) {
       const int rl = idx / NVMAX, qo = idx - rl * NVMAX;
-      const int r = r_lo + rl;
-      const int ax = r / n, j = r - ax * n;
+      const int axj = rowt[rl];
+      const int ax = axj >> 16, j = axj & 0xffff;
       double cv;
       if (mode == 0) {
         cv = qo < p.nv ? p.c0[((long long)ax * n + j) * p.nv + qo] : 0.0;
@@ -646,16 +662,22 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
       if (lane == 0 && bmx > 0.0) atomicMax(cx.bnd + (k % 3), (unsigned long long)__double_as_longlong(bmx));
     }
     // 4. positions
+    int t = start >> 16, rl = start & 0xffff;
     for (int idx = threadIdx.x; idx < nr * m; idx += LG_NT) {
-      const int t = idx / nr, rl = idx - t * nr;
-      const int r = r_lo + rl;
-      const int ax = r / n, j = r - ax * n;
+      const int axj = rowt[rl];
+      const int ax = axj >> 16, j = axj & 0xffff;
       const double* pr = Ps + t * NVMAX;
       const double* cj = cr + rl * NVMAX;
       double v = 0.0;
 #pragma unroll
       for (int q = 0; q < NVMAX; ++q) v = fma(pr[q], cj[q], v);
       cx.X[((long long)t * 3 + ax) * p.npad + j] = v;
+      t += dt;
+      rl += drl;
+      if (rl >= nr) {
+        rl -= nr;
+        ++t;
+      }
     }
     stamp(tsr, 10);
   }
@@ -667,7 +689,7 @@ __device__ __forceinline__ void lg_rows(const LgParams& p, const LgCtx& cx, unsi
     int cnt[LG_MAXB];
 #pragma unroll
     for (int b = 0; b < LG_MAXB; ++b) cnt[b] = 0;
-    for (int r = r_lo; r < r_hi; ++r) cnt[(r % n) >> 5]++;
+    for (int rl = 0; rl < nr; ++rl) cnt[(rowt[rl] & 0xffff) >> 5]++;
     __threadfence();
 #pragma unroll
     for (int b = 0; b < LG_MAXB; ++b)
@@ -719,6 +741,25 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
     for (int j = 0; j < n; ++j) s += p.beq[((long long)ax * n + j) * 6 + e];
     bbar[threadIdx.x] = s / n;
   }
+  {
+    // R-phase row indices of this CTA (LG_RT_*), once per launch
+    int* rt = reinterpret_cast<int*>(smb + L.rows);
+    const int R3 = 3 * n;
+    const int r_lo = (int)((long long)cx.cta * R3 / p.cpg), r_hi = (int)((long long)(cx.cta + 1) * R3 / p.cpg);
+    const int nr = r_hi - r_lo;
+    if (threadIdx.x == 0) {
+      rt[0] = r_lo;
+      rt[1] = r_hi;
+      rt[2] = nr;
+      rt[3] = nr ? LG_NT / nr : 0;
+      rt[4] = nr ? LG_NT % nr : 0;
+    }
+    rt[LG_RT_START + threadIdx.x] = nr ? ((int)(threadIdx.x / nr) << 16) | (int)(threadIdx.x % nr) : 0;
+    for (int rl = threadIdx.x; rl < nr; rl += LG_NT) {
+      const int r = r_lo + rl;
+      rt[LG_RT_ROW + rl] = ((r / n) << 16) | (r % n);
+    }
+  }
   double* misc = reinterpret_cast<double*>(smb + L.misc);
   __syncthreads();
   const bool sphere = cx.lxy == cx.lz;
@@ -738,11 +779,16 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
 
   int prev_stage = -1, iters = 0, conv = 0;
   const long long xstride = 3LL * n * NVMAX + 4;
+  int st_q = 0, st_r = 0;  // k = st_q * switch_every + st_r, kept without a division
   for (int k = 0;; ++k) {
     long long* tsr = (ts && k < 256) ? ts + 16 * k : nullptr;
     stamp(tsr, 0);
-    const int stage = min(k / p.switch_every, p.S - 1);
-    const int stage_n = min((k + 1) / p.switch_every, p.S - 1);
+    if (k > 0 && ++st_r == p.switch_every) {
+      st_r = 0;
+      ++st_q;
+    }
+    const int stage = min(st_q, p.S - 1);
+    const int stage_n = min(st_q + (st_r + 1 == p.switch_every ? 1 : 0), p.S - 1);
     if (stage != prev_stage) {
       double* mat = reinterpret_cast<double*>(smb + L.mat);
       for (int i = threadIdx.x; i < SM::SIZE; i += LG_NT) mat[i] = p.mats[(long long)stage * SM::SIZE + i];
