@@ -492,7 +492,23 @@ __device__ __forceinline__ void lg_pair_phase(const LgParams& p, const LgCtx& cx
 __device__ __forceinline__ void lg_norms(const double* slots, int count, double& s2, double& mx) {
   const int lane = threadIdx.x & 31;
   double a = 0.0, b = 0.0;
-  for (int i = lane; i < count; i += 32) {
+  // every slot load in flight at once (one L2 round trip, not one per 32 slots), then the same
+  // lane-ordered sums
+  constexpr int U = 8;  // 256 slots: every CTA of a launch
+  double va[U], vb[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = lane + 32 * u;
+    va[u] = i < count ? __ldcg(slots + 2 * i) : 0.0;
+    vb[u] = i < count ? __ldcg(slots + 2 * i + 1) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (lane + 32 * u < count) {
+      a += va[u];
+      b = fmax(b, vb[u]);
+    }
+  for (int i = lane + 32 * U; i < count; i += 32) {
     a += __ldcg(slots + 2 * i);
     b = fmax(b, __ldcg(slots + 2 * i + 1));
   }
