@@ -134,7 +134,8 @@ __host__ __device__ inline LgSmem lg_smem(int m, int chunk_rows) {
   s.xs = take(LG_NW * 96 * 8);
   s.P = take(m * NVMAX * 8);
   s.mat = take(StageMats<NVMAX>::SIZE * 8);
-  s.blist = take(LG_MAXB * LG_MAXB * 4 + (LG_MAXB * (LG_MAXB + 1) / 2 + 1) * 4);
+  // per-block slot lists | ab_first (nab + 1) | ab_pair (2 nab)
+  s.blist = take(LG_MAXB * LG_MAXB * 4 + (LG_MAXB * (LG_MAXB + 1) / 2 + 1) * 4 + LG_MAXB * (LG_MAXB + 1) * 4);
   s.bbar = take(18 * 8);
   s.misc = take(8 * 8 + LG_MAXB * 4);  // broadcast words + per-block seen epochs
   s.rows = take((LG_RT_ROW + LG_ROWS_MAX) * 4);  // R-phase row indices (see LG_RT_*)
@@ -417,7 +418,8 @@ __device__ __forceinline__ void lg_pair_phase(const LgParams& p, const LgCtx& cx
   for (int u = u0 + warp; u < u1; u += LG_NW) {
     int ab = 0;
     while (abf[ab + 1] <= u) ++ab;
-    const int A = p.ab_pair[2 * ab], B = p.ab_pair[2 * ab + 1];
+    const int* abp = abf + LG_MAXB * (LG_MAXB + 1) / 2 + 1;  // ab_pair in smem (one L2 trip less per unit)
+    const int A = abp[2 * ab], B = abp[2 * ab + 1];
     const bool diag = A == B;
     const int lu = u - abf[ab];
     const int t = diag ? lu : (lu >> 1), h = diag ? 0 : (lu & 1);
@@ -750,6 +752,8 @@ __global__ void __launch_bounds__(LG_NT, 1) am_large_kernel(const LgParams p)
     for (; e < LG_MAXB; ++e) blist[b * LG_MAXB + e] = -1;
   }
   for (int i = threadIdx.x; i <= p.nab; i += LG_NT) blist[LG_MAXB * LG_MAXB + i] = p.ab_first[i];
+  for (int i = threadIdx.x; i < 2 * p.nab; i += LG_NT)
+    blist[LG_MAXB * LG_MAXB + LG_MAXB * (LG_MAXB + 1) / 2 + 1 + i] = p.ab_pair[i];
   double* bbar = reinterpret_cast<double*>(smb + L.bbar);
   if (threadIdx.x < 18) {
     const int ax = threadIdx.x / 6, e = threadIdx.x - 6 * ax;
