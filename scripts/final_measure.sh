@@ -8,7 +8,7 @@ python bench.py --impl reference > $OUT/bench_reference.jsonl 2> $OUT/bench_refe
 python bench.py --steps 2 --warmup 3 --no-cpu --no-single > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu --no-single > $OUT/ncu_launch.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:am_cluster -c 1 -o /tmp/final_full \
+ncu --set full --import-source on --clock-control none -k regex:am_cluster -c 1 -f -o /tmp/final_full \
     python bench.py --steps 1 --warmup 3 --no-cpu --no-single > $OUT/ncu_full.log 2>&1
 ncu -i /tmp/final_full.ncu-rep --page raw --csv 2>/dev/null | gzip > $OUT/full_raw.csv.gz
 ncu -i /tmp/final_full.ncu-rep --page details --csv 2>/dev/null | gzip > $OUT/full_details.csv.gz
