@@ -32,7 +32,7 @@ EXPORTS = ("st_plan_create", "st_plan_destroy", "st_solve", "st_solve_report", "
            "st_solve_report_begin", "st_solve_end")
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()  # re-entrant: load() is reachable from GC finalizers (_PinnedPool)
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -117,7 +117,9 @@ class _PinnedPool:
 
     def __init__(self, keep: int = 4):
         self._free: dict = {}
-        self._lock = threading.Lock()
+        # re-entrant: _release runs as a weakref finalizer, i.e. from the garbage collector, which
+        # can fire on any allocation -- including one made while this thread holds the lock
+        self._lock = threading.RLock()
         self._keep = keep
 
     def empty(self, shape, dtype=np.float64) -> np.ndarray:
@@ -136,8 +138,9 @@ class _PinnedPool:
         return np.frombuffer(raw, dtype=dtype, count=count).reshape(shape)
 
     def _release(self, ptr: int, nbytes: int) -> None:
+        fresh = []  # allocated before taking the lock
         with self._lock:
-            bucket = self._free.setdefault(nbytes, [])
+            bucket = self._free.setdefault(nbytes, fresh)
             if len(bucket) < self._keep:
                 bucket.append(ptr)
                 return

@@ -361,3 +361,23 @@ def test_disk_cache_roundtrip(tmp_path):
     broken = kkt.FactorCache(disk_dir=tmp_path)
     broken.get(fp, basis, 1.0)
     assert broken.stats()["factorizations"] == 1
+
+
+def test_pinned_pool_release_is_reentrant():
+    """The pool's release runs as a weakref finalizer, i.e. from the garbage collector, which can
+    fire inside the pool's own critical section: releasing with the lock held must not deadlock."""
+    import threading
+
+    from paper_2011_04240_b200 import native
+    pool = native._PinnedPool(keep=4)
+    done = []
+
+    def run():
+        with pool._lock:
+            pool._release(0x1000, 64)  # a finalizer firing while the lock is held
+        done.append(True)
+
+    t = threading.Thread(target=run, daemon=True)
+    t.start()
+    t.join(5.0)
+    assert done == [True] and pool._free[64] == [0x1000]
